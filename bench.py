@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""Driver benchmark: the D3Q19 binary-fluid full timestep on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], and configs[4] at N > 1): one full
+timestep = pull streaming + order parameter phi + chemical potential mu
+(7-point stencil) + Guo-forced binary collision, fp64, periodic, 256^3 sites
+per GPU (weak scaling: z-slabs of 256 planes per rank, NCCL halos).  A "step"
+is one timestep of the whole lattice.  Inputs: reference random_binary_state
+per slab (kernels.py:216-227), synthetic.  State (2 x 2 x 2.55 GB per GPU) is
+far larger than L2, so no L2 flush is needed between steps.
+
+Prints ONE JSON line on rank 0.  `value` = lattice site updates/s (MLUPS) of
+the whole job with the state resident in HBM; `e2e` = the same metric through
+the public API with host buffers (H2D of the step's input state, the step,
+D2H of its result state, every step); `roofline` = the dominant kernel
+(k_collide_stream) timed with CUDA events on its stream inside the timed
+region against the measured HBM copy bandwidth; `cpu_baseline` = the oracle
+port (oracle/lb_oracle.c, OpenMP, all host threads) on a bounded sample.
+
+--impl reference times the CPU implementation of the same step (the oracle
+port of the path: the reference package is Python-only, cannot travel to the
+GPU box and has no streaming/free-energy step at all) on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+#: algorithmic bytes per site update: read f,g 2*19*8 + mu 8, write f,g 2*19*8
+CS_BYTES_PER_SITE = 616
+#: whole step: phi (read g 152 + write 8) + mu (read 8 + write 8) + collide-stream 616
+STEP_BYTES_PER_SITE = 792
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--shape", default="256x256x256", help="per-GPU lattice NXxNYxNZ")
+    p.add_argument("--mode", choices=("exact", "fast"), default="exact")
+    p.add_argument("--vvl", type=int, default=1)
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--seed", type=int, default=1234)
+    return p.parse_args(argv)
+
+
+# ----------------------------------------------------------------- helpers
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class Control:
+    """Control plane over torch.distributed (gloo): barriers, max, broadcast.
+    The halo data path is the engine's own NCCL communicator."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.dist = None
+        if world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo")
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def allreduce(self, value: float, op: str) -> float:
+        if not self.dist:
+            return value
+        import torch
+
+        t = torch.tensor([value], dtype=torch.float64)
+        self.dist.all_reduce(t, op=getattr(self.dist.ReduceOp, op))
+        return float(t.item())
+
+    def bcast_bytes(self, data: bytes | None, n: int) -> bytes:
+        if not self.dist:
+            return data
+        import torch
+
+        t = torch.zeros(n, dtype=torch.uint8)
+        if data is not None:
+            t[:] = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        self.dist.broadcast(t, src=0)
+        return bytes(t.numpy().tobytes())
+
+    def close(self):
+        if self.dist:
+            self.dist.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax.append(float(parts[2]))
+                    power.append(float(parts[3]))
+                except ValueError:
+                    continue
+                for name, flag in zip(names, parts[5:9]):
+                    if flag.lower() == "active":
+                        reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "power_w_max": max(power) if power else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def measured_hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(shape_key: str):
+    """dram bytes per k_collide_stream launch from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            data = json.load(fh)
+        entry = data.get(shape_key) or {}
+        return entry.get("k_collide_stream_dram_bytes")
+    except Exception:
+        return None
+
+
+def cpu_oracle_rate(shape, steps, seed, threads=None):
+    """Oracle port (lb_oracle.c orc_fluid_step, OpenMP) on a host lattice: MLUPS."""
+    from oracle import oracle as orc
+
+    nx, ny, nz = shape
+    n = nx * ny * nz
+    p = -(-n // 16) * 16
+    f, g = orc.random_binary_state(n, p, seed)
+    prm = orc.fluid_params(tau_f=1.0, tau_g=1.0, physics=1)
+    if threads is None:
+        threads = os.cpu_count() or 1
+    orc.set_threads(threads)
+    orc.fluid_step(f, g, shape, p, prm, steps=1)  # warm-up (page faults, thread pool)
+    t0 = time.perf_counter()
+    orc.fluid_step(f, g, shape, p, prm, steps=steps)
+    dt = time.perf_counter() - t0
+    return n * steps / dt / 1e6, threads, dt
+
+
+# ----------------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    nx, ny, _ = (int(v) for v in args.shape.lower().split("x"))
+    sample = (nx, ny, 32)
+    steps = max(1, args.steps)
+    from oracle import oracle as orc
+
+    n = sample[0] * sample[1] * sample[2]
+    p = -(-n // 16) * 16
+    f, g = orc.random_binary_state(n, p, args.seed)
+    prm = orc.fluid_params(tau_f=1.0, tau_g=1.0, physics=1)
+    threads = os.cpu_count() or 1
+    orc.set_threads(threads)
+    for _ in range(max(1, args.warmup)):
+        f, g, _, _ = orc.fluid_step(f, g, sample, p, prm, steps=1)
+    t0 = time.perf_counter()
+    f, g, _, _ = orc.fluid_step(f, g, sample, p, prm, steps=steps)
+    dt = time.perf_counter() - t0
+    mlups = n * steps / dt / 1e6
+    line = {
+        "impl": "reference",
+        "metric": "lattice site updates/sec (MLUPS), D3Q19 binary-fluid full timestep",
+        "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": dt / steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"full timestep {args.shape} per GPU (sample {sample[0]}x"
+                               f"{sample[1]}x{sample[2]} on the host)",
+                   "shape_per_gpu": args.shape, "physics": "binary free energy"},
+        "cpu_baseline": {"value": mlups, "unit": "MLUPS", "cores": threads, "kind": "port",
+                         "sample": f"{sample[0]}x{sample[1]}x{sample[2]} periodic lattice, "
+                                   f"{steps} timesteps (oracle/lb_oracle.c orc_fluid_step)"},
+        "e2e": {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local):
+    import ctypes
+
+    import paper_1405_6162_b200 as lk
+    from paper_1405_6162_b200 import _native as nat
+    from paper_1405_6162_b200.kernels import random_binary_state
+
+    ctl = Control(world)
+    nat.check(nat.lib.ltk_set_device(local))
+    nx, ny, nzl = (int(v) for v in args.shape.lower().split("x"))
+    shape = lk.LatticeShape(nx, ny, nzl * world)
+    mode = lk.MODE_FAST if args.mode == "fast" else lk.MODE_EXACT
+    model = lk.D3Q19Model(tau_f=1.0, tau_g=1.0)
+    sim = lk.BinaryFluid(shape, model=model, physics="binary", mode=mode, vvl=args.vvl,
+                         rank=rank, nranks=world, device=local, use_graph=False)
+    if world > 1:
+        uid = lk.nccl_unique_id() if rank == 0 else None
+        sim.attach_nccl(ctl.bcast_bytes(uid, 128))
+
+    # per-slab synthetic state in reference order (x*ny + y)*nzl + z
+    slab_shape = lk.LatticeShape(nx, ny, nzl)
+    f0, g0 = random_binary_state(slab_shape, np.random.default_rng(args.seed + rank), model)
+    sim.load(f0, g0)
+    sites_rank = nx * ny * nzl
+
+    launches0 = nat.launch_count()
+    sim.run(args.warmup)
+    sim.sync()
+    ctl.barrier()
+
+    start, stop = nat.event_create(True), nat.event_create(True)
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    ctl.barrier()
+    sim.sync()
+    l_before = nat.launch_count()
+    sim.profile(True)
+    nat.check(nat.lib.ltk_event_record(start, sim.stream))
+    sim.run(args.steps)
+    nat.check(nat.lib.ltk_event_record(stop, sim.stream))
+    sim.sync()
+    prof = sim.profile(False)
+    ms = nat.elapsed_ms(start, stop)
+    launches = nat.launch_count() - l_before
+    ctl.barrier()
+    clk = clocks.stop() if rank == 0 else None
+    ms_max = ctl.allreduce(ms, "MAX")
+    launches_all = int(ctl.allreduce(float(launches), "SUM"))
+
+    total_sites = sites_rank * world
+    value = total_sites * args.steps / (ms_max * 1e-3) / 1e6  # MLUPS
+
+    # dominant kernel: k_collide_stream (all planes) -- prof[2] covers it
+    cs_ms = prof[2] / args.steps
+    peak, peak_src = measured_hbm_peak()
+    achieved = CS_BYTES_PER_SITE * sites_rank / (cs_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(args.shape if world == 1 else f"{args.shape}/p{world}")
+    roofline = {"bound": "hbm", "kernel": "k_collide_stream", "achieved": achieved,
+                "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peak_src,
+                "bytes_per_site": CS_BYTES_PER_SITE,
+                "kernel_ms_per_step": cs_ms,
+                "share_of_step": prof[2] / max(prof[3], 1e-9),
+                "phi_ms_per_step": prof[0] / args.steps,
+                "mu_ms_per_step": prof[1] / args.steps,
+                "full_step_frac": STEP_BYTES_PER_SITE * sites_rank / (ms / args.steps * 1e-3)
+                / 1e9 / peak}
+
+    # ---------------- e2e: public API with host buffers, every step
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, sim, f0, g0, ctl, world, nat, lk)
+
+    # ---------------- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = (nx, ny, 16)
+        rate, threads, dt = cpu_oracle_rate(sample, 3, args.seed)
+        cpu = {"value": rate, "unit": "MLUPS", "cores": threads, "kind": "port",
+               "sample": f"{sample[0]}x{sample[1]}x{sample[2]} periodic lattice, 3 timesteps "
+                         f"({dt:.1f} s), oracle/lb_oracle.c orc_fluid_step"}
+
+    sim.close()
+    if rank == 0:
+        line = {
+            "metric": "lattice site updates/sec (MLUPS), D3Q19 binary-fluid full timestep",
+            "value": value, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "full timestep (stream + phi + mu + forced collision), "
+                                   f"{args.shape} per GPU, z-slabs" +
+                                   (" (BASELINE configs[2])" if world == 1 else
+                                    " (BASELINE configs[4], weak scaling)"),
+                       "lattice": f"{nx}x{ny}x{nzl * world}", "shape_per_gpu": args.shape,
+                       "mode": args.mode, "vvl": args.vvl, "physics": "binary free energy",
+                       "l2": "state 10.2 GB/GPU >> 126 MB L2, no flush needed",
+                       "parallelism": f"z-slab x{world}"},
+            "gpu_launches": launches_all,
+            "clocks": clk,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    ctl.close()
+    return 0
+
+
+def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
+    """Public-API path with host buffers: per step H2D state -> load (transpose)
+    -> 1 timestep -> store (transpose) -> D2H state, pinned host memory."""
+    import ctypes
+
+    from paper_1405_6162_b200.memory import pinned_empty
+
+    nelem = f0.data.size
+    nb = 8 * nelem
+    hf, hg = pinned_empty(nelem), pinned_empty(nelem)
+    hf[:] = f0.data
+    hg[:] = g0.data
+    of, og = pinned_empty(nelem), pinned_empty(nelem)
+    stage = nat.malloc(2 * nb)
+    padded = f0.descriptor.padded_sites
+    nzl = sim.nzl
+    st = sim.stream
+
+    def one_step():
+        nat.check(nat.lib.ltk_h2d(stage, hf.ctypes.data, nb, st))
+        nat.check(nat.lib.ltk_h2d(stage + nb, hg.ctypes.data, nb, st))
+        sim.load_device(stage, stage + nb, padded, nzl, 0, st)
+        sim.run(1)
+        sim.store_device(stage, stage + nb, padded, nzl, 0, st)
+        nat.check(nat.lib.ltk_d2h(of.ctypes.data, stage, nb, st))
+        nat.check(nat.lib.ltk_d2h(og.ctypes.data, stage + nb, nb, st))
+
+    one_step()
+    sim.sync()
+    ctl.barrier()
+    t0 = time.perf_counter()
+    start, stop = nat.event_create(True), nat.event_create(True)
+    nat.check(nat.lib.ltk_event_record(start, st))
+    for _ in range(args.e2e_steps):
+        one_step()
+    nat.check(nat.lib.ltk_event_record(stop, st))
+    sim.sync()
+    ms = nat.elapsed_ms(start, stop)
+    ms_max = ctl.allreduce(ms, "MAX")
+    nat.free(stage)
+    sites = sim.shape.nx * sim.shape.ny * nzl * world
+    return {"value": sites * args.e2e_steps / (ms_max * 1e-3) / 1e6, "unit": "MLUPS",
+            "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
+            "steps": args.e2e_steps, "ms_per_step": ms_max / args.e2e_steps,
+            "path": "H2D(f,g pinned) -> BinaryFluid load -> run(1) -> store -> D2H(f,g)"}
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    rank, world, local = dist_env()
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

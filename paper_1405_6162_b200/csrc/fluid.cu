@@ -1,0 +1,832 @@
+// fluid.cu -- the full D3Q19 binary-fluid timestep on B200: C-ABI launchers
+// of the kernels in fluid_kernels.cuh, host-order <-> slab transposes, halo
+// faces, and the C++ step engine (single GPU periodic, or z-slabs with NCCL
+// halo exchange overlapped with the interior planes).
+//
+// No reference counterpart (reference pkg/README.md:34-35: collision only);
+// specification in DESIGN.md §2-§5.  The collision arithmetic is the
+// reference's (kernels.py:89-125) with the free-energy force terms added.
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is dlopen'ed at run time
+
+#include <algorithm>
+#include <cstring>
+#include <initializer_list>
+#include <new>
+#include <vector>
+
+#include "fluid_kernels.cuh"
+
+namespace ltk {
+
+// ------------------------------------------------------------------ helpers
+
+static int check_slab(const ltk_slab *s, int vvl) {
+    if (!s || s->nx < 1 || s->ny < 1 || s->nzl < 1)
+        return fail(LTK_ERR_SHAPE, "invalid slab extents");
+    if (s->cstride < (s->nzl + 2) * s->nx * s->ny)
+        return fail(LTK_ERR_SHAPE, "cstride %lld < (nzl+2)*nx*ny", (long long)s->cstride);
+    if (vvl != 1 && vvl != 2 && vvl != 4)
+        return fail(LTK_ERR_PLAN, "fluid kernels support vvl 1, 2, 4 (got %d)", vvl);
+    if (s->nx % vvl) return fail(LTK_ERR_PLAN, "vvl %d does not divide nx %lld", vvl,
+                                 (long long)s->nx);
+    if ((s->nx * s->ny) % 2 || s->cstride % 2)
+        return fail(LTK_ERR_SHAPE, "nx*ny and cstride must be even (16-byte vector rows)");
+    if ((long long)s->nx * s->ny * (s->nzl + 2) >= (1LL << 31))
+        return fail(LTK_ERR_SHAPE, "slab too large for 32-bit thread indexing");
+    return LTK_OK;
+}
+
+static void fill_args(FluidArgs &a, const ltk_slab *s, const ltk_fluid_params *p) {
+    memset(&a, 0, sizeof a);
+    a.nx = (int)s->nx;
+    a.ny = (int)s->ny;
+    a.nzl = (int)s->nzl;
+    a.PL = s->nx * s->ny;
+    a.cstride = s->cstride;
+    a.nz_global = s->nzl;
+    a.z0 = 0;
+    if (p) {
+        for (int i = 0; i < Q; ++i) {
+            a.wv[i] = p->wv[i];
+            a.lam[i] = p->lam[i];
+        }
+        a.cs2 = p->cs2;
+        a.tau_f = p->tau_f;
+        a.tau_g = p->tau_g;
+        a.A = p->A;
+        a.B = p->B;
+        a.kappa = p->kappa;
+        a.gamma = p->gamma;
+        a.c1 = 2.0 * p->cs2;
+        a.c2 = a.c1 * p->cs2;
+        a.cs2sq = p->cs2 * p->cs2;
+        a.srcpre = 1.0 - 0.5 / p->tau_f;
+        a.inv_tau_f = 1.0 / p->tau_f;
+        a.inv_tau_g = 1.0 / p->tau_g;
+        a.a1 = 1.0 / p->cs2;
+        a.a2 = 1.0 / a.c2;
+        a.a3 = 1.0 / a.c1;
+        a.inv_cs2 = 1.0 / p->cs2;
+        a.inv_cs2sq = 1.0 / a.cs2sq;
+    }
+}
+
+static void set_planes(FluidArgs &a, int vvl, long long z_lo, long long z_hi) {
+    a.z_lo = (int)z_lo;
+    a.nplanes = (int)(z_hi - z_lo);
+    a.nthreads = (long long)a.nplanes * a.ny * (a.nx / vvl);
+}
+
+static inline unsigned grid_for(long long n, int tpb) { return (unsigned)((n + tpb - 1) / tpb); }
+
+constexpr int kTPB = 128;
+
+static int launch_phi(const FluidArgs &a, int vvl, cudaStream_t st) {
+    if (a.nthreads <= 0) return LTK_OK;
+    const unsigned g = grid_for(a.nthreads, kTPB);
+    switch (vvl) {
+        case 1: k_phi<1><<<g, kTPB, 0, st>>>(a); break;
+        case 2: k_phi<2><<<g, kTPB, 0, st>>>(a); break;
+        default: k_phi<4><<<g, kTPB, 0, st>>>(a); break;
+    }
+    LTK_CHECK_LAUNCH("k_phi");
+    return LTK_OK;
+}
+
+static int launch_mu(const FluidArgs &a, int vvl, cudaStream_t st) {
+    if (a.nthreads <= 0) return LTK_OK;
+    const unsigned g = grid_for(a.nthreads, kTPB);
+    switch (vvl) {
+        case 1: k_mu<1><<<g, kTPB, 0, st>>>(a); break;
+        case 2: k_mu<2><<<g, kTPB, 0, st>>>(a); break;
+        default: k_mu<4><<<g, kTPB, 0, st>>>(a); break;
+    }
+    LTK_CHECK_LAUNCH("k_mu");
+    return LTK_OK;
+}
+
+template <int MODE, int PHYS>
+static void launch_cs_t(const FluidArgs &a, int vvl, cudaStream_t st) {
+    const unsigned g = grid_for(a.nthreads, kTPB);
+    if (vvl == 2)
+        k_collide_stream<2, MODE, PHYS><<<g, kTPB, 0, st>>>(a);
+    else
+        k_collide_stream<1, MODE, PHYS><<<g, kTPB, 0, st>>>(a);
+}
+
+static int launch_cs(const FluidArgs &a, int vvl, int mode, int phys, cudaStream_t st) {
+    if (a.nthreads <= 0) return LTK_OK;
+    if (vvl > 2) return fail(LTK_ERR_PLAN, "collide-stream supports vvl 1, 2 (got %d)", vvl);
+    if (mode == LTK_MODE_EXACT && phys == 1) launch_cs_t<LTK_MODE_EXACT, 1>(a, vvl, st);
+    else if (mode == LTK_MODE_EXACT) launch_cs_t<LTK_MODE_EXACT, 0>(a, vvl, st);
+    else if (phys == 1) launch_cs_t<LTK_MODE_FAST, 1>(a, vvl, st);
+    else launch_cs_t<LTK_MODE_FAST, 0>(a, vvl, st);
+    LTK_CHECK_LAUNCH("k_collide_stream");
+    return LTK_OK;
+}
+
+// ------------------------------------------------------------------ plane copies
+struct PlaneCopies {
+    const double *src[24];
+    double *dst[24];
+    int n;
+    long long PL;
+};
+
+__global__ void __launch_bounds__(256) k_plane_copy(const PlaneCopies pc) {
+    const int j = blockIdx.y;
+    const double2 *s = reinterpret_cast<const double2 *>(pc.src[j]);
+    double2 *d = reinterpret_cast<double2 *>(pc.dst[j]);
+    const long long n2 = pc.PL / 2;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
+         i += (long long)gridDim.x * blockDim.x)
+        d[i] = s[i];
+}
+
+static int run_plane_copies(const PlaneCopies &pc, cudaStream_t st) {
+    if (pc.n == 0) return LTK_OK;
+    dim3 grid((unsigned)std::min<long long>((pc.PL / 2 + 255) / 256, 148 * 4), pc.n);
+    k_plane_copy<<<grid, 256, 0, st>>>(pc);
+    LTK_CHECK_LAUNCH("k_plane_copy");
+    return LTK_OK;
+}
+
+constexpr int kUp[5] = {5, 11, 13, 15, 17};    // cz = +1
+constexpr int kDown[5] = {6, 12, 14, 16, 18};  // cz = -1
+
+static inline double *plane(double *base, const ltk_slab *s, int comp, long long zs) {
+    return base + comp * s->cstride + zs * s->nx * s->ny;
+}
+
+// ------------------------------------------------------------------ transposes
+// host order site (x*ny + y)*nzg + z  <->  slab (z - z0 + 1)*PL + y*nx + x.
+// 32x32 (x, z) tiles staged in shared memory, both sides coalesced.
+template <bool TO_SLAB>
+__global__ void __launch_bounds__(256) k_transpose(double *slab, double *host, long long nx,
+                                                   long long ny, long long nzl, long long nzg,
+                                                   long long z0, long long padded,
+                                                   long long cstride, int ncomp) {
+    __shared__ double tile[32][33];
+    const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
+    const long long xb = (long long)blockIdx.x * 32, zb = (long long)blockIdx.y * 32;
+    const long long yc = blockIdx.z;
+    const long long y = yc % ny;
+    const int c = (int)(yc / ny);
+    if (c >= ncomp) return;
+    double *h = host + (long long)c * padded;
+    double *sl = slab + (long long)c * cstride;
+    const long long PL = nx * ny;
+    if (TO_SLAB) {
+        for (int k = ty; k < 32; k += 8) {  // read host: z fastest
+            const long long x = xb + k, z = zb + tx;
+            if (x < nx && z < nzl) tile[k][tx] = h[(x * ny + y) * nzg + z0 + z];
+        }
+        __syncthreads();
+        for (int k = ty; k < 32; k += 8) {  // write slab: x fastest
+            const long long x = xb + tx, z = zb + k;
+            if (x < nx && z < nzl) sl[(z + 1) * PL + y * nx + x] = tile[tx][k];
+        }
+    } else {
+        for (int k = ty; k < 32; k += 8) {
+            const long long x = xb + tx, z = zb + k;
+            if (x < nx && z < nzl) tile[tx][k] = sl[(z + 1) * PL + y * nx + x];
+        }
+        __syncthreads();
+        for (int k = ty; k < 32; k += 8) {
+            const long long x = xb + k, z = zb + tx;
+            if (x < nx && z < nzl) h[(x * ny + y) * nzg + z0 + z] = tile[k][tx];
+        }
+    }
+}
+
+static int transpose(const ltk_slab *s, double *slab, double *host, long long padded,
+                     long long nzg, long long z0, int ncomp, bool to_slab, cudaStream_t st) {
+    if (z0 < 0 || z0 + s->nzl > nzg) return fail(LTK_ERR_SHAPE, "slab planes outside lattice");
+    if (padded < s->nx * s->ny * nzg) return fail(LTK_ERR_SHAPE, "padded < nsites");
+    if ((long long)s->ny * ncomp > 65535LL * 65535LL) return fail(LTK_ERR_SHAPE, "too many rows");
+    dim3 block(32, 8);
+    dim3 grid((unsigned)((s->nx + 31) / 32), (unsigned)((s->nzl + 31) / 32),
+              (unsigned)(s->ny * ncomp));
+    if (grid.z > 65535) return fail(LTK_ERR_SHAPE, "ny*ncomp exceeds 65535");
+    if (to_slab)
+        k_transpose<true><<<grid, block, 0, st>>>(slab, host, s->nx, s->ny, s->nzl, nzg, z0,
+                                                  padded, s->cstride, ncomp);
+    else
+        k_transpose<false><<<grid, block, 0, st>>>(slab, host, s->nx, s->ny, s->nzl, nzg, z0,
+                                                   padded, s->cstride, ncomp);
+    LTK_CHECK_LAUNCH("k_transpose");
+    return LTK_OK;
+}
+
+// ------------------------------------------------------------------ masked pack
+__global__ void k_pack_sites(const double *src, double *packed, const long long *idx,
+                             long long k, int ncomp, long long padded, int unpack) {
+    const long long n = k * ncomp;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long c = t / k, j = t - c * k;
+        const long long e = c * padded + idx[j];
+        if (unpack)
+            const_cast<double *>(src)[e] = packed[t];
+        else
+            packed[t] = src[e];
+    }
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct Nccl {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+
+static Nccl &nccl() {
+    static Nccl n;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!n.h) n.h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (n.h) {
+            n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.h, "ncclGetUniqueId");
+            n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.h, "ncclCommInitRank");
+            n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
+            n.GroupStart = (decltype(n.GroupStart))dlsym(n.h, "ncclGroupStart");
+            n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.h, "ncclGroupEnd");
+            n.Send = (decltype(n.Send))dlsym(n.h, "ncclSend");
+            n.Recv = (decltype(n.Recv))dlsym(n.h, "ncclRecv");
+            n.GetErrorString = (decltype(n.GetErrorString))dlsym(n.h, "ncclGetErrorString");
+            n.ok = n.GetUniqueId && n.CommInitRank && n.CommDestroy && n.GroupStart &&
+                   n.GroupEnd && n.Send && n.Recv && n.GetErrorString;
+        }
+    }
+    return n;
+}
+
+#define LTK_NCCL(call)                                                                 \
+    do {                                                                               \
+        ncclResult_t r_ = (call);                                                      \
+        if (r_ != ncclSuccess)                                                         \
+            return fail(LTK_ERR_DEVICE, "%s: %s", #call, nccl().GetErrorString(r_));    \
+    } while (0)
+
+}  // namespace ltk
+
+// ------------------------------------------------------------------ engine
+struct ltk_fluid {
+    int dev = 0;
+    long long nx = 0, ny = 0, nzg = 0, nzl = 0, z0 = 0;
+    int rank = 0, nranks = 1, vvl = 1;
+    ltk_fluid_params prm{};
+    ltk_slab slab{};
+    double *fg[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [state][f/g]
+    double *phi = nullptr, *mu = nullptr;
+    int cur = 0;
+    cudaStream_t st = nullptr, comm_st = nullptr;
+    cudaEvent_t ev_fork[3] = {}, ev_join[3] = {};
+    ncclComm_t comm = nullptr;
+    bool use_graph = false;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    bool prof = false;
+    cudaEvent_t pev[5] = {};          // events of the step being enqueued
+    std::vector<cudaEvent_t> ppool;   // 4 per profiled step, read at the end
+    long long prof_steps = 0;
+};
+
+namespace ltk {
+
+static void drop_graphs(ltk_fluid *e) {
+    for (auto &g : e->gexec)
+        if (g) {
+            cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+}
+
+static FluidArgs engine_args(const ltk_fluid *e, int in_state) {
+    FluidArgs a;
+    fill_args(a, &e->slab, &e->prm);
+    a.nz_global = e->nzg;
+    a.z0 = e->z0;
+    a.f_in = e->fg[in_state][0];
+    a.g_in = e->fg[in_state][1];
+    a.f_out = e->fg[1 - in_state][0];
+    a.g_out = e->fg[1 - in_state][1];
+    a.phi_in = e->phi;
+    a.phi_out = e->phi;
+    a.mu = e->mu;
+    a.mu_out = e->mu;
+    a.err = singular_word();
+    a.wrap = (e->nranks == 1 && e->comm == nullptr) ? 1 : 0;
+    return a;
+}
+
+// One NCCL halo exchange group on comm_st.  kind 0: f/g crossing components
+// of state `s`; kind 1: phi; kind 2: mu.  Send order per peer is fixed
+// (faces up, then faces down) and receive order mirrors it, which keeps the
+// matching right even when both neighbours are the same rank (P = 2) or
+// this rank itself (P = 1).
+static int exchange(ltk_fluid *e, int kind, int s) {
+    Nccl &n = nccl();
+    const int up = (e->rank + 1) % e->nranks, down = (e->rank + e->nranks - 1) % e->nranks;
+    const size_t PL = (size_t)(e->nx * e->ny);
+    const long long top = e->nzl, bot = 1, halo_lo = 0, halo_hi = e->nzl + 1;
+    const ltk_slab *sl = &e->slab;
+    LTK_NCCL(n.GroupStart());
+    if (kind == 0) {
+        for (int d = 0; d < 2; ++d)
+            for (int j = 0; j < 5; ++j)
+                LTK_NCCL(n.Send(plane(e->fg[s][d], sl, kUp[j], top), PL, ncclFloat64, up, e->comm,
+                                e->comm_st));
+        for (int d = 0; d < 2; ++d)
+            for (int j = 0; j < 5; ++j)
+                LTK_NCCL(n.Send(plane(e->fg[s][d], sl, kDown[j], bot), PL, ncclFloat64, down,
+                                e->comm, e->comm_st));
+        for (int d = 0; d < 2; ++d)
+            for (int j = 0; j < 5; ++j)
+                LTK_NCCL(n.Recv(plane(e->fg[s][d], sl, kUp[j], halo_lo), PL, ncclFloat64, down,
+                                e->comm, e->comm_st));
+        for (int d = 0; d < 2; ++d)
+            for (int j = 0; j < 5; ++j)
+                LTK_NCCL(n.Recv(plane(e->fg[s][d], sl, kDown[j], halo_hi), PL, ncclFloat64, up,
+                                e->comm, e->comm_st));
+    } else {
+        double *b = kind == 1 ? e->phi : e->mu;
+        LTK_NCCL(n.Send(b + top * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
+        LTK_NCCL(n.Send(b + bot * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
+        LTK_NCCL(n.Recv(b + halo_lo * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
+        LTK_NCCL(n.Recv(b + halo_hi * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
+    }
+    LTK_NCCL(n.GroupEnd());
+    return LTK_OK;
+}
+
+#define LTK_RC(x)              \
+    do {                       \
+        int rc_ = (x);         \
+        if (rc_) return rc_;   \
+    } while (0)
+
+// Enqueue one timestep reading state `s` and writing state 1 - s.
+static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
+    FluidArgs a = engine_args(e, s);
+    const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
+    const long long nzl = e->nzl;
+    if (prof) cudaEventRecord(e->pev[0], st);
+    if (e->comm == nullptr) {
+        // single slab, periodic z: three kernels, halos written by the kernels
+        set_planes(a, vvl, 0, nzl);
+        LTK_RC(launch_phi(a, vvl, st));
+        if (prof) cudaEventRecord(e->pev[1], st);
+        if (phys == 1) LTK_RC(launch_mu(a, vvl, st));
+        if (prof) cudaEventRecord(e->pev[2], st);
+        LTK_RC(launch_cs(a, vvl, mode, phys, st));
+        if (prof) cudaEventRecord(e->pev[3], st);
+        return LTK_OK;
+    }
+    // z-slabs: each exchange overlaps the interior planes of the next kernel
+    const long long in_lo = 1, in_hi = nzl - 1;  // interior (may be empty)
+    auto boundary = [&](auto launch_one) -> int {
+        set_planes(a, vvl, 0, 1);
+        LTK_RC(launch_one());
+        if (nzl > 1) {
+            set_planes(a, vvl, nzl - 1, nzl);
+            LTK_RC(launch_one());
+        }
+        return LTK_OK;
+    };
+    // (1) f/g faces || phi interior
+    LTK_CUDA(cudaEventRecord(e->ev_fork[0], st));
+    LTK_CUDA(cudaStreamWaitEvent(e->comm_st, e->ev_fork[0], 0));
+    LTK_RC(exchange(e, 0, s));
+    LTK_CUDA(cudaEventRecord(e->ev_join[0], e->comm_st));
+    if (in_hi > in_lo) {
+        set_planes(a, vvl, in_lo, in_hi);
+        LTK_RC(launch_phi(a, vvl, st));
+    }
+    LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[0], 0));
+    LTK_RC(boundary([&] { return launch_phi(a, vvl, st); }));
+    if (prof) cudaEventRecord(e->pev[1], st);
+    if (phys == 1) {
+        // (2) phi faces || mu interior
+        LTK_CUDA(cudaEventRecord(e->ev_fork[1], st));
+        LTK_CUDA(cudaStreamWaitEvent(e->comm_st, e->ev_fork[1], 0));
+        LTK_RC(exchange(e, 1, s));
+        LTK_CUDA(cudaEventRecord(e->ev_join[1], e->comm_st));
+        if (in_hi > in_lo) {
+            set_planes(a, vvl, in_lo, in_hi);
+            LTK_RC(launch_mu(a, vvl, st));
+        }
+        LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[1], 0));
+        LTK_RC(boundary([&] { return launch_mu(a, vvl, st); }));
+        // (3) mu faces || collide-stream interior
+        LTK_CUDA(cudaEventRecord(e->ev_fork[2], st));
+        LTK_CUDA(cudaStreamWaitEvent(e->comm_st, e->ev_fork[2], 0));
+        LTK_RC(exchange(e, 2, s));
+        LTK_CUDA(cudaEventRecord(e->ev_join[2], e->comm_st));
+    }
+    if (prof) cudaEventRecord(e->pev[2], st);
+    if (in_hi > in_lo) {
+        set_planes(a, vvl, in_lo, in_hi);
+        LTK_RC(launch_cs(a, vvl, mode, phys, st));
+    }
+    if (phys == 1) LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[2], 0));
+    LTK_RC(boundary([&] { return launch_cs(a, vvl, mode, phys, st); }));
+    if (prof) cudaEventRecord(e->pev[3], st);
+    return LTK_OK;
+}
+
+static int wrap_state_halos(ltk_fluid *e, int s, int which, cudaStream_t st) {
+    return ltk_fluid_wrap_halos(&e->slab, e->fg[s][0], e->fg[s][1], e->phi, e->mu, which, st);
+}
+
+}  // namespace ltk
+
+using namespace ltk;
+
+extern "C" {
+
+int ltk_fluid_phi(const ltk_slab *s, const double *g, double *phi, int64_t z_lo, int64_t z_hi,
+                  void *stream) {
+    LTK_RC(check_slab(s, 1));
+    if (z_lo < 0 || z_hi > s->nzl || z_hi < z_lo) return fail(LTK_ERR_BOUNDS, "plane range");
+    FluidArgs a;
+    fill_args(a, s, nullptr);
+    a.g_in = g;
+    a.phi_out = phi;
+    set_planes(a, 1, z_lo, z_hi);
+    return launch_phi(a, 1, as_stream(stream));
+}
+
+int ltk_fluid_mu(const ltk_slab *s, const double *phi, double *mu, const ltk_fluid_params *p,
+                 int64_t z_lo, int64_t z_hi, void *stream) {
+    LTK_RC(check_slab(s, 1));
+    if (z_lo < 0 || z_hi > s->nzl || z_hi < z_lo) return fail(LTK_ERR_BOUNDS, "plane range");
+    FluidArgs a;
+    fill_args(a, s, p);
+    a.phi_in = phi;
+    a.mu_out = mu;
+    set_planes(a, 1, z_lo, z_hi);
+    return launch_mu(a, 1, as_stream(stream));
+}
+
+int ltk_fluid_collide_stream(const ltk_slab *s, const double *f_in, const double *g_in,
+                             const double *mu, double *f_out, double *g_out,
+                             const ltk_fluid_params *p, int64_t z_lo, int64_t z_hi, int32_t vvl,
+                             void *stream) {
+    LTK_RC(check_slab(s, vvl));
+    if (!p) return fail(LTK_ERR_CONFIG, "null params");
+    if (z_lo < 0 || z_hi > s->nzl || z_hi < z_lo) return fail(LTK_ERR_BOUNDS, "plane range");
+    FluidArgs a;
+    fill_args(a, s, p);
+    a.f_in = f_in;
+    a.g_in = g_in;
+    a.mu = mu;
+    a.f_out = f_out;
+    a.g_out = g_out;
+    a.err = singular_word();
+    set_planes(a, vvl, z_lo, z_hi);
+    return launch_cs(a, vvl, p->mode, p->physics, as_stream(stream));
+}
+
+int ltk_fluid_wrap_halos(const ltk_slab *s, double *f, double *g, double *phi, double *mu,
+                         int32_t which, void *stream) {
+    LTK_RC(check_slab(s, 1));
+    PlaneCopies pc;
+    memset(&pc, 0, sizeof pc);
+    pc.PL = s->nx * s->ny;
+    const long long nzl = s->nzl;
+    if (which & 1) {
+        for (int j = 0; j < 5; ++j) {
+            for (double *b : {f, g}) {
+                pc.src[pc.n] = plane(b, s, kUp[j], nzl);
+                pc.dst[pc.n++] = plane(b, s, kUp[j], 0);
+                pc.src[pc.n] = plane(b, s, kDown[j], 1);
+                pc.dst[pc.n++] = plane(b, s, kDown[j], nzl + 1);
+            }
+        }
+    }
+    for (int k = 0; k < 2; ++k) {
+        double *b = k == 0 ? phi : mu;
+        if (!(which & (2 << k)) || !b) continue;
+        pc.src[pc.n] = b + nzl * pc.PL;
+        pc.dst[pc.n++] = b;
+        pc.src[pc.n] = b + pc.PL;
+        pc.dst[pc.n++] = b + (nzl + 1) * pc.PL;
+    }
+    return run_plane_copies(pc, as_stream(stream));
+}
+
+int ltk_fluid_pack_face(const ltk_slab *s, const double *f, const double *g, double *buf,
+                        int32_t dir, void *stream) {
+    LTK_RC(check_slab(s, 1));
+    if (dir != 1 && dir != -1) return fail(LTK_ERR_CONFIG, "dir must be +1 or -1");
+    PlaneCopies pc;
+    memset(&pc, 0, sizeof pc);
+    pc.PL = s->nx * s->ny;
+    const int *comps = dir > 0 ? kUp : kDown;
+    const long long zs = dir > 0 ? s->nzl : 1;
+    for (int d = 0; d < 2; ++d)
+        for (int j = 0; j < 5; ++j) {
+            pc.src[pc.n] = plane(const_cast<double *>(d ? g : f), s, comps[j], zs);
+            pc.dst[pc.n] = buf + (long long)pc.n * pc.PL;
+            ++pc.n;
+        }
+    return run_plane_copies(pc, as_stream(stream));
+}
+
+int ltk_fluid_unpack_face(const ltk_slab *s, double *f, double *g, const double *buf,
+                          int32_t dir, void *stream) {
+    LTK_RC(check_slab(s, 1));
+    if (dir != 1 && dir != -1) return fail(LTK_ERR_CONFIG, "dir must be +1 or -1");
+    PlaneCopies pc;
+    memset(&pc, 0, sizeof pc);
+    pc.PL = s->nx * s->ny;
+    const int *comps = dir > 0 ? kUp : kDown;
+    const long long zs = dir > 0 ? 0 : s->nzl + 1;
+    for (int d = 0; d < 2; ++d)
+        for (int j = 0; j < 5; ++j) {
+            pc.src[pc.n] = buf + (long long)pc.n * pc.PL;
+            pc.dst[pc.n] = plane(d ? g : f, s, comps[j], zs);
+            ++pc.n;
+        }
+    return run_plane_copies(pc, as_stream(stream));
+}
+
+int ltk_fluid_scatter(const ltk_slab *s, const double *host, int64_t padded, int64_t nz_global,
+                      int64_t z0, int32_t ncomp, double *slab, void *stream) {
+    LTK_RC(check_slab(s, 1));
+    return transpose(s, slab, const_cast<double *>(host), padded, nz_global, z0, ncomp, true,
+                     as_stream(stream));
+}
+
+int ltk_fluid_gather(const ltk_slab *s, const double *slab, int64_t padded, int64_t nz_global,
+                     int64_t z0, int32_t ncomp, double *host, void *stream) {
+    LTK_RC(check_slab(s, 1));
+    return transpose(s, const_cast<double *>(slab), host, padded, nz_global, z0, ncomp, false,
+                     as_stream(stream));
+}
+
+int ltk_pack_sites(const double *src, double *packed, const int64_t *idx, int64_t k,
+                   int32_t ncomp, int64_t padded, void *stream) {
+    if (k <= 0) return LTK_OK;
+    const long long n = k * ncomp;
+    const unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_pack_sites<<<g, 256, 0, as_stream(stream)>>>(src, packed, (const long long *)idx, k, ncomp,
+                                                   padded, 0);
+    LTK_CHECK_LAUNCH("k_pack_sites");
+    return LTK_OK;
+}
+
+int ltk_unpack_sites(double *dst, const double *packed, const int64_t *idx, int64_t k,
+                     int32_t ncomp, int64_t padded, void *stream) {
+    if (k <= 0) return LTK_OK;
+    const long long n = k * ncomp;
+    const unsigned g = (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_pack_sites<<<g, 256, 0, as_stream(stream)>>>(dst, const_cast<double *>(packed),
+                                                   (const long long *)idx, k, ncomp, padded, 1);
+    LTK_CHECK_LAUNCH("k_unpack_sites");
+    return LTK_OK;
+}
+
+// ---------------------------------------------------------------- engine API
+
+int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank, int32_t nranks,
+                     const ltk_fluid_params *p, int32_t vvl, ltk_fluid **out) {
+    *out = nullptr;
+    if (!p) return fail(LTK_ERR_CONFIG, "null params");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return fail(LTK_ERR_CONFIG, "bad rank/nranks");
+    if (nz_global % nranks)
+        return fail(LTK_ERR_SHAPE, "nz %lld not divisible by %d ranks", (long long)nz_global,
+                    nranks);
+    if (p->tau_f <= 0.5 || p->tau_g <= 0.5) return fail(LTK_ERR_CONFIG, "tau must be > 0.5");
+    if (p->mode != LTK_MODE_EXACT && p->mode != LTK_MODE_FAST)
+        return fail(LTK_ERR_CONFIG, "unknown mode %d", p->mode);
+    if (p->physics != 0 && p->physics != 1) return fail(LTK_ERR_CONFIG, "unknown physics");
+    ltk_fluid *e = new (std::nothrow) ltk_fluid();
+    if (!e) return fail(LTK_ERR_ALLOC, "host allocation failed");
+    e->nx = nx;
+    e->ny = ny;
+    e->nzg = nz_global;
+    e->nzl = nz_global / nranks;
+    e->z0 = (long long)rank * e->nzl;
+    e->rank = rank;
+    e->nranks = nranks;
+    e->vvl = vvl;
+    e->prm = *p;
+    e->slab.nx = nx;
+    e->slab.ny = ny;
+    e->slab.nzl = e->nzl;
+    // component stride: whole planes, rounded up to 64 doubles (512 B)
+    const long long raw = (e->nzl + 2) * nx * ny;
+    e->slab.cstride = (raw + 63) / 64 * 64;
+    int rc = check_slab(&e->slab, vvl);
+    if (!rc && vvl > 2) rc = fail(LTK_ERR_PLAN, "engine vvl must be 1 or 2");
+    if (rc) {
+        delete e;
+        return rc;
+    }
+    cudaGetDevice(&e->dev);
+    const size_t dist_bytes = (size_t)e->slab.cstride * Q * sizeof(double);
+    const size_t plane_bytes = (size_t)raw * sizeof(double);
+    void *ptr = nullptr;
+    for (int s = 0; s < 2; ++s)
+        for (int d = 0; d < 2; ++d) {
+            rc = ltk_malloc(&ptr, dist_bytes);
+            if (rc) {
+                ltk_fluid_destroy(e);
+                return rc;
+            }
+            e->fg[s][d] = (double *)ptr;
+        }
+    if ((rc = ltk_malloc(&ptr, plane_bytes))) {
+        ltk_fluid_destroy(e);
+        return rc;
+    }
+    e->phi = (double *)ptr;
+    if ((rc = ltk_malloc(&ptr, plane_bytes))) {
+        ltk_fluid_destroy(e);
+        return rc;
+    }
+    e->mu = (double *)ptr;
+    if (cudaStreamCreateWithFlags(&e->st, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&e->comm_st, cudaStreamNonBlocking) != cudaSuccess) {
+        ltk_fluid_destroy(e);
+        return fail(LTK_ERR_DEVICE, "stream creation failed");
+    }
+    for (int k = 0; k < 3; ++k) {
+        cudaEventCreateWithFlags(&e->ev_fork[k], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&e->ev_join[k], cudaEventDisableTiming);
+    }
+    if (!singular_word()) {
+        ltk_fluid_destroy(e);
+        return fail(LTK_ERR_DEVICE, "device error word unavailable");
+    }
+    *out = e;
+    return LTK_OK;
+}
+
+int ltk_fluid_destroy(ltk_fluid *e) {
+    if (!e) return LTK_OK;
+    if (e->st) cudaStreamSynchronize(e->st);
+    if (e->comm_st) cudaStreamSynchronize(e->comm_st);
+    drop_graphs(e);
+    if (e->comm && nccl().ok) nccl().CommDestroy(e->comm);
+    for (auto &s : e->fg)
+        for (auto &p : s)
+            if (p) cudaFree(p);
+    if (e->phi) cudaFree(e->phi);
+    if (e->mu) cudaFree(e->mu);
+    for (int k = 0; k < 3; ++k) {
+        if (e->ev_fork[k]) cudaEventDestroy(e->ev_fork[k]);
+        if (e->ev_join[k]) cudaEventDestroy(e->ev_join[k]);
+    }
+    for (auto ev : e->ppool) cudaEventDestroy(ev);
+    if (e->st) cudaStreamDestroy(e->st);
+    if (e->comm_st) cudaStreamDestroy(e->comm_st);
+    delete e;
+    return LTK_OK;
+}
+
+int ltk_fluid_slab(const ltk_fluid *e, ltk_slab *s, int64_t *z0) {
+    *s = e->slab;
+    if (z0) *z0 = e->z0;
+    return LTK_OK;
+}
+
+int ltk_fluid_buffers(const ltk_fluid *e, double **f, double **g, double **phi, double **mu) {
+    if (f) *f = e->fg[e->cur][0];
+    if (g) *g = e->fg[e->cur][1];
+    if (phi) *phi = e->phi;
+    if (mu) *mu = e->mu;
+    return LTK_OK;
+}
+
+int ltk_fluid_stream(const ltk_fluid *e, void **stream) {
+    *stream = e->st;
+    return LTK_OK;
+}
+
+int ltk_fluid_set_params(ltk_fluid *e, const ltk_fluid_params *p) {
+    if (p->tau_f <= 0.5 || p->tau_g <= 0.5) return fail(LTK_ERR_CONFIG, "tau must be > 0.5");
+    e->prm = *p;
+    drop_graphs(e);
+    return LTK_OK;
+}
+
+int ltk_fluid_load(ltk_fluid *e, const double *f_src, const double *g_src, int64_t padded,
+                   int64_t nz_src, int64_t z_src0, void *stream) {
+    cudaStream_t st = stream ? as_stream(stream) : e->st;
+    e->cur = 0;
+    LTK_RC(ltk_fluid_scatter(&e->slab, f_src, padded, nz_src, z_src0, Q, e->fg[0][0], st));
+    LTK_RC(ltk_fluid_scatter(&e->slab, g_src, padded, nz_src, z_src0, Q, e->fg[0][1], st));
+    if (e->comm == nullptr) LTK_RC(wrap_state_halos(e, 0, 1, st));
+    return LTK_OK;
+}
+
+int ltk_fluid_store(ltk_fluid *e, double *f_dst, double *g_dst, int64_t padded, int64_t nz_src,
+                    int64_t z_src0, void *stream) {
+    cudaStream_t st = stream ? as_stream(stream) : e->st;
+    LTK_RC(ltk_fluid_gather(&e->slab, e->fg[e->cur][0], padded, nz_src, z_src0, Q, f_dst, st));
+    LTK_RC(ltk_fluid_gather(&e->slab, e->fg[e->cur][1], padded, nz_src, z_src0, Q, g_dst, st));
+    return LTK_OK;
+}
+
+int ltk_fluid_use_graph(ltk_fluid *e, int32_t enable) {
+    drop_graphs(e);
+    e->use_graph = enable != 0;
+    return LTK_OK;
+}
+
+// Profiling: every profiled step records 4 events (start, after phi, after
+// mu + halo, after collide-stream) on the engine stream; nothing waits on
+// them until the window is read, so the timed stream runs undisturbed.
+int ltk_fluid_profile(ltk_fluid *e, int32_t enable, float *ms4) {
+    float acc[4] = {0, 0, 0, 0};
+    if (!e->ppool.empty()) {
+        LTK_CUDA(cudaEventSynchronize(e->ppool.back()));
+        for (size_t k = 0; k + 3 < e->ppool.size(); k += 4) {
+            float ms;
+            cudaEventElapsedTime(&ms, e->ppool[k], e->ppool[k + 1]);
+            acc[0] += ms;
+            cudaEventElapsedTime(&ms, e->ppool[k + 1], e->ppool[k + 2]);
+            acc[1] += ms;
+            cudaEventElapsedTime(&ms, e->ppool[k + 2], e->ppool[k + 3]);
+            acc[2] += ms;
+            cudaEventElapsedTime(&ms, e->ppool[k], e->ppool[k + 3]);
+            acc[3] += ms;
+        }
+        for (auto ev : e->ppool) cudaEventDestroy(ev);
+        e->ppool.clear();
+    }
+    if (ms4)
+        for (int k = 0; k < 4; ++k) ms4[k] = acc[k];
+    e->prof = enable != 0;
+    e->prof_steps = 0;
+    return LTK_OK;
+}
+
+int ltk_fluid_run(ltk_fluid *e, int64_t nsteps, void *stream) {
+    cudaStream_t st = stream ? as_stream(stream) : e->st;
+    for (int64_t k = 0; k < nsteps; ++k) {
+        const int s = e->cur;
+        if (e->prof) {
+            for (int k = 0; k < 4; ++k) {
+                cudaEvent_t ev;
+                LTK_CUDA(cudaEventCreate(&ev));
+                e->ppool.push_back(ev);
+                e->pev[k] = ev;
+            }
+            LTK_RC(enqueue_step(e, s, st, true));
+            ++e->prof_steps;
+        } else if (e->use_graph && e->comm == nullptr) {
+            if (!e->gexec[s]) {
+                cudaGraph_t g;
+                LTK_CUDA(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
+                int rc = enqueue_step(e, s, e->st, false);
+                cudaError_t ce = cudaStreamEndCapture(e->st, &g);
+                if (rc) return rc;
+                if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+                ce = cudaGraphInstantiate(&e->gexec[s], g, 0);
+                cudaGraphDestroy(g);
+                if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+            }
+            LTK_CUDA(cudaGraphLaunch(e->gexec[s], st));
+            count_launch(3);
+        } else {
+            LTK_RC(enqueue_step(e, s, st, false));
+        }
+        e->cur = 1 - s;
+    }
+    return LTK_OK;
+}
+
+int ltk_nccl_available(void) { return nccl().ok ? 1 : 0; }
+
+int ltk_nccl_unique_id(char id[128]) {
+    if (!nccl().ok) return fail(LTK_ERR_DEVICE, "libnccl.so.2 not loadable");
+    ncclUniqueId u;
+    LTK_NCCL(nccl().GetUniqueId(&u));
+    memcpy(id, u.internal, 128);
+    return LTK_OK;
+}
+
+int ltk_fluid_attach_nccl(ltk_fluid *e, const char id[128]) {
+    if (!nccl().ok) return fail(LTK_ERR_DEVICE, "libnccl.so.2 not loadable");
+    ncclUniqueId u;
+    memcpy(u.internal, id, 128);
+    LTK_NCCL(nccl().CommInitRank(&e->comm, e->nranks, u, e->rank));
+    drop_graphs(e);
+    return LTK_OK;
+}
+
+}  // extern "C"

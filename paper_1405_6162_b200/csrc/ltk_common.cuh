@@ -1,0 +1,148 @@
+// ltk_common.cuh -- shared helpers of libltk.so (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <type_traits>
+
+#include "ltk.h"
+
+namespace ltk {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+int fail(int status, const char *fmt, ...);
+int cuda_fail(cudaError_t err, const char *what);
+void count_launch(int n = 1);
+
+#define LTK_CUDA(call)                                        \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return ltk::cuda_fail(e_, #call); \
+    } while (0)
+
+#define LTK_CHECK_LAUNCH(what)                                  \
+    do {                                                        \
+        cudaError_t e_ = cudaGetLastError();                    \
+        if (e_ != cudaSuccess) return ltk::cuda_fail(e_, what); \
+        ltk::count_launch();                                    \
+    } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Device error word: lowest real site with rho <= 0 (INT64_MAX = none).
+// Defined in runtime.cu; declared extern for the kernels (relocatable code
+// is not used, so kernels call ltk::flag_singular via a pointer obtained at
+// launch time).
+long long *singular_word();
+
+__device__ __forceinline__ void flag_singular(long long *word, long long site) {
+    atomicMin(reinterpret_cast<unsigned long long *>(word),
+              static_cast<unsigned long long>(site));
+}
+
+// ---------------------------------------------------------------- D3Q19
+// Canonical ordering of reference model.py:21-34.
+constexpr int Q = 19;
+__host__ __device__ constexpr int cx(int i) {
+    constexpr int t[Q] = {0, 1, -1, 0, 0, 0, 0, 1, 1, -1, -1, 1, 1, -1, -1, 0, 0, 0, 0};
+    return t[i];
+}
+__host__ __device__ constexpr int cy(int i) {
+    constexpr int t[Q] = {0, 0, 0, 1, -1, 0, 0, 1, -1, 1, -1, 0, 0, 0, 0, 1, 1, -1, -1};
+    return t[i];
+}
+__host__ __device__ constexpr int cz(int i) {
+    constexpr int t[Q] = {0, 0, 0, 0, 0, 1, -1, 0, 0, 0, 0, 1, -1, 1, -1, 1, -1, 1, -1};
+    return t[i];
+}
+
+// Sum of ci*u over the nonzero velocity components, in x, y, z order.  The
+// reference evaluates ((ux*cx + uy*cy) + uz*cz) with cx..cz in {0, +-1}:
+// products by +-1 are exact and adding a +-0 product never changes a value
+// (SURVEY.md Appendix B), so dropping zero terms is bitwise neutral.
+template <int CX, int CY, int CZ, class M>
+__device__ __forceinline__ double dot_c(double ux, double uy, double uz) {
+    double acc = 0.0;
+    bool first = true;
+    if (CX != 0) { acc = CX > 0 ? ux : -ux; first = false; }
+    if (CY != 0) {
+        double t = CY > 0 ? uy : -uy;
+        acc = first ? t : M::add(acc, t);
+        first = false;
+    }
+    if (CZ != 0) {
+        double t = CZ > 0 ? uz : -uz;
+        acc = first ? t : M::add(acc, t);
+        first = false;
+    }
+    return acc;
+}
+
+// Compile-time loop over the 19 velocities: f(std::integral_constant-like).
+template <int I>
+struct Int {
+    static constexpr int value = I;
+};
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (I < N) {
+        f(Int<I>{});
+        static_for<I + 1, N>(f);
+    }
+}
+
+// ---------------------------------------------------------------- arithmetic
+// EXACT: one IEEE round-to-nearest op per call, never contracted to FMA.
+struct Exact {
+    static constexpr bool exact = true;
+    __device__ static __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+    __device__ static __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+    __device__ static __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    __device__ static __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+};
+
+// FAST: plain operators (the compiler may contract to FMA).
+struct Fast {
+    static constexpr bool exact = false;
+    __device__ static __forceinline__ double add(double a, double b) { return a + b; }
+    __device__ static __forceinline__ double sub(double a, double b) { return a - b; }
+    __device__ static __forceinline__ double mul(double a, double b) { return a * b; }
+    __device__ static __forceinline__ double div(double a, double b) { return a / b; }
+};
+
+// Vector load/store of VVL consecutive doubles (VVL*8-byte aligned).
+template <int VVL>
+struct Vec {
+    double v[VVL];
+};
+
+template <int VVL>
+__device__ __forceinline__ void load_vec(double (&dst)[VVL], const double *p) {
+    if constexpr (VVL == 1) {
+        dst[0] = __ldg(p);
+    } else {
+#pragma unroll
+        for (int k = 0; k < VVL; k += 2) {
+            double2 t = __ldg(reinterpret_cast<const double2 *>(p + k));
+            dst[k] = t.x;
+            dst[k + 1] = t.y;
+        }
+    }
+}
+
+template <int VVL>
+__device__ __forceinline__ void store_vec(double *p, const double (&src)[VVL]) {
+    if constexpr (VVL == 1) {
+        p[0] = src[0];
+    } else {
+#pragma unroll
+        for (int k = 0; k < VVL; k += 2)
+            *reinterpret_cast<double2 *>(p + k) = make_double2(src[k], src[k + 1]);
+    }
+}
+
+}  // namespace ltk

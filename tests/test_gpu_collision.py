@@ -1,0 +1,267 @@
+"""GPU parity of the reference hot path: the D3Q19 binary collision through
+the reference-facing API (TargetDevice / launch / sync_target -> ltk_collide).
+
+Bar: bitwise equal to the reference (EXACT mode) on the golden vectors that
+the reference itself produced (tests/golden/), and to the oracle on fresh
+inputs; FAST mode within 1e-12 relative.  Reference tests mirrored:
+test_kernels.py:157-214, test_acceptance.py:56-101.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def lk():
+    import paper_1405_6162_b200 as lk
+
+    return lk
+
+
+def _state(lk, shape, seed, model=None):
+    from paper_1405_6162_b200.kernels import random_binary_state
+
+    return random_binary_state(lk.LatticeShape(*shape), np.random.default_rng(seed),
+                               model or lk.D3Q19Model())
+
+
+class TestGoldenParity:
+    @pytest.mark.parametrize("vvl", [1, 2, 4, 8, 16])
+    def test_all_golden_cases_bitwise(self, lk, golden, vvl):
+        from paper_1405_6162_b200.verify import run_framework_collision
+
+        meta, _ = golden
+        for case in meta["collision"]:
+            if case["padded"] % vvl:
+                continue
+            model = lk.D3Q19Model(tau_f=case["tau_f"], tau_g=case["tau_g"])
+            f0, g0 = _state(lk, case["shape"], case["seed"], model)
+            assert sha(f0.data) == case["in_f"]
+            f1, g1 = run_framework_collision(f0, g0, "cuda", vvl, 1, steps=case["steps"],
+                                             model=model)
+            assert sha(f1.data) == case["out_f"], (case["shape"], vvl)
+            assert sha(g1.data) == case["out_g"], (case["shape"], vvl)
+
+    @pytest.mark.parametrize("tpb", [32, 64, 256])
+    def test_tpb_independent(self, lk, golden, tpb):
+        from paper_1405_6162_b200.verify import run_framework_collision
+
+        meta, _ = golden
+        case = meta["collision"][2]  # 16^3
+        model = lk.D3Q19Model(tau_f=case["tau_f"], tau_g=case["tau_g"])
+        f0, g0 = _state(lk, case["shape"], case["seed"], model)
+        f1, g1 = run_framework_collision(f0, g0, "cuda", 2, 1, steps=case["steps"], model=model,
+                                         tpb=tpb)
+        assert sha(f1.data) == case["out_f"] and sha(g1.data) == case["out_g"]
+
+    def test_fast_mode_within_1e12(self, lk):
+        from oracle import oracle as orc
+        from paper_1405_6162_b200.verify import run_framework_collision
+
+        model = lk.D3Q19Model(tau_f=0.8, tau_g=1.3)
+        f0, g0 = _state(lk, (32, 32, 32), 99, model)
+        f1, g1 = run_framework_collision(f0, g0, "cuda", 2, 1, steps=10, model=model,
+                                         mode=lk.MODE_FAST)
+        rf, rg = f0.data.copy(), g0.data.copy()
+        orc.collide(rf, rg, f0.descriptor.padded_sites, 32 ** 3, tau_f=0.8, tau_g=1.3, steps=10)
+        for got, ref in ((f1.data, rf), (g1.data, rg)):
+            rel = np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300))
+            assert rel <= 1e-12, rel
+
+    def test_large_lattice_bitwise_vs_oracle(self, lk):
+        # 128^3, BASELINE configs[1], against the oracle (itself pinned bitwise)
+        from oracle import oracle as orc
+        from paper_1405_6162_b200.verify import run_framework_collision
+
+        model = lk.D3Q19Model(tau_f=0.8, tau_g=1.0)
+        f0, g0 = _state(lk, (128, 128, 128), 1234, model)
+        f1, g1 = run_framework_collision(f0, g0, "cuda", 1, 1, steps=2, model=model)
+        rf, rg = f0.data.copy(), g0.data.copy()
+        orc.collide(rf, rg, f0.descriptor.padded_sites, 128 ** 3, tau_f=0.8, tau_g=1.0, steps=2,
+                    threads=8)
+        assert np.array_equal(f1.data, rf) and np.array_equal(g1.data, rg)
+
+
+class TestContracts:
+    def test_singular_state_surfaces_at_sync(self, lk):
+        # reference test_kernels.py:187-197
+        desc = lk.FieldDescriptor.create(19, 8, max_vvl=8)
+        dev = lk.TargetDevice()
+        lk.set_model_constants(dev, lk.D3Q19Model())
+        bf, bg = lk.target_malloc(dev, desc), lk.target_malloc(dev, desc)
+        lk.launch(dev, lk.binary_collision_kernel, lk.LaunchPlan(extent=desc.padded_sites, vvl=8),
+                  [bf, bg])
+        with pytest.raises(lk.SingularStateError):
+            lk.sync_target(dev)
+        lk.sync_target(dev)  # error consumed
+
+    def test_padding_untouched(self, lk):
+        from paper_1405_6162_b200.verify import run_framework_collision
+
+        f0, g0 = _state(lk, (3, 3, 3), 6)
+        for vvl in (1, 2, 4, 8, 16):
+            f1, g1 = run_framework_collision(f0, g0, "cuda", vvl, 1)
+            P = f0.descriptor.padded_sites
+            for i in range(19):
+                assert not f1.data[i * P + 27:(i + 1) * P].any()
+                assert not g1.data[i * P + 27:(i + 1) * P].any()
+
+    def test_equilibrium_fixed_point_and_conservation(self, lk):
+        from paper_1405_6162_b200.verify import verify_conservation, verify_fixed_point
+
+        ok, lines = verify_fixed_point(lk.LatticeShape(8, 8, 8))
+        assert ok, lines
+        ok, lines = verify_conservation(lk.LatticeShape(16, 16, 16), seed=20140709)
+        assert ok, lines
+
+    def test_verify_suite(self, lk):
+        from paper_1405_6162_b200.verify import run_verify_suite
+
+        ok, lines = run_verify_suite("binary-collision", lk.LatticeShape(8, 8, 8))
+        assert ok, lines
+
+    def test_descriptor_mismatch_and_missing_constant(self, lk):
+        dev = lk.TargetDevice()
+        lk.set_model_constants(dev, lk.D3Q19Model())
+        bf = lk.target_malloc(dev, lk.FieldDescriptor.create(19, 16))
+        bg = lk.target_malloc(dev, lk.FieldDescriptor.create(19, 32))
+        with pytest.raises(lk.ShapeError):
+            lk.launch(dev, lk.binary_collision_kernel, lk.LaunchPlan(extent=16, vvl=4), [bf, bg])
+        dev2 = lk.TargetDevice()
+        b1 = lk.target_malloc(dev2, lk.FieldDescriptor.create(19, 16))
+        b2 = lk.target_malloc(dev2, lk.FieldDescriptor.create(19, 16))
+        with pytest.raises(lk.ConfigError):
+            lk.launch(dev2, lk.binary_collision_kernel, lk.LaunchPlan(extent=16, vvl=4), [b1, b2])
+
+    def test_noncanonical_cv_rejected(self, lk):
+        dev = lk.TargetDevice()
+        lk.set_model_constants(dev, lk.D3Q19Model())
+        cv = lk.D3Q19Model().cvf[::-1].copy()
+        dev.constant_set_double_array("cv", cv, (19, 3))
+        b1 = lk.target_malloc(dev, lk.FieldDescriptor.create(19, 16))
+        b2 = lk.target_malloc(dev, lk.FieldDescriptor.create(19, 16))
+        with pytest.raises(lk.ConfigError):
+            lk.launch(dev, lk.binary_collision_kernel, lk.LaunchPlan(extent=16, vvl=4), [b1, b2])
+
+    def test_debug_device_write_tracking(self, lk):
+        from paper_1405_6162_b200.verify import run_framework_collision
+
+        f0, g0 = _state(lk, (4, 4, 2), 7)
+        plain = run_framework_collision(f0, g0, "cuda", 4, 1)
+        tracked = run_framework_collision(f0, g0, "cuda", 4, 1, debug=True)
+        assert np.array_equal(plain[0].data, tracked[0].data)
+        assert np.array_equal(plain[1].data, tracked[1].data)
+
+    def test_python_kernel_rejected_on_device(self, lk):
+        dev = lk.TargetDevice()
+        buf = lk.target_malloc(dev, lk.FieldDescriptor.create(1, 8, max_vvl=8))
+        with pytest.raises(lk.ConfigError):
+            lk.launch(dev, lk.python_kernel("noop", lambda ctx: None),
+                      lk.LaunchPlan(extent=8, vvl=8), [buf])
+
+
+class TestScaleAndMemory:
+    def test_scale_bitwise(self, lk, golden):
+        from paper_1405_6162_b200.verify import run_framework_scale
+
+        _, small = golden
+        d = lk.FieldDescriptor.create(3, 60)
+        base = lk.Field(d, small["scale_5x4x3_in"].copy())
+        for vvl in (1, 2, 4, 8, 16):
+            out = run_framework_scale(base, 0.37, "cuda", vvl)
+            assert np.array_equal(out.data, small["scale_5x4x3_out"])
+
+    def test_round_trip_and_zero_init(self, lk):
+        dev = lk.TargetDevice()
+        desc = lk.FieldDescriptor.create(3, 11)
+        buf = lk.target_malloc(dev, desc)
+        out = lk.field_create(desc)
+        lk.copy_from_target(out, buf)
+        assert not out.data.any()
+        f = lk.field_create(desc)
+        f.data[:] = np.random.default_rng(5).random(desc.nelem)
+        lk.copy_to_target(buf, f)
+        lk.copy_from_target(out, buf)
+        assert np.array_equal(out.data, f.data)
+        lk.target_free(buf)
+        with pytest.raises(lk.LifecycleError):
+            lk.target_free(buf)
+        with pytest.raises(lk.LifecycleError):
+            lk.copy_to_target(buf, f)
+
+    def test_masked_copies_vs_reference_vectors(self, lk, golden):
+        _, small = golden
+        dev = lk.TargetDevice()
+        k = 0
+        while f"mask{k}_flags" in small:
+            ncomp, nsites, padded = (int(v) for v in small[f"mask{k}_meta"])
+            desc = lk.FieldDescriptor.create(ncomp, nsites, max_vvl=8)
+            assert desc.padded_sites == padded
+            buf = lk.target_malloc(dev, desc)
+            lk.copy_to_target(buf, lk.Field(desc, small[f"mask{k}_init"].copy()))
+            flags = small[f"mask{k}_flags"]
+            before = dev.counters.elements_packed
+            lk.copy_to_target_masked(buf, lk.Field(desc, small[f"mask{k}_host"].copy()),
+                                     lk.SiteMask(flags))
+            assert dev.counters.elements_packed - before == int(flags.sum()) * ncomp
+            out = lk.field_create(desc)
+            lk.copy_from_target(out, buf)
+            assert np.array_equal(out.data, small[f"mask{k}_out"])
+            # and back: masked D2H onto a random host field
+            host = lk.Field(desc, np.random.default_rng(k).random(desc.nelem))
+            expect = host.data.copy()
+            from oracle import oracle as orc
+            orc.masked_copy(expect, out.data, ncomp, padded, flags)
+            lk.copy_from_target_masked(host, buf, lk.SiteMask(flags))
+            assert np.array_equal(host.data, expect)
+            lk.target_free(buf)
+            k += 1
+
+    def test_isolation_uncopied_reads_zero(self, lk):
+        dev = lk.TargetDevice()
+        desc = lk.FieldDescriptor.create(19, 64)
+        bf, bg = lk.target_malloc(dev, desc), lk.target_malloc(dev, desc)
+        host = lk.field_create(desc)
+        lk.copy_from_target(host, bf)
+        assert not host.data.any()
+
+    def test_in_flight_guard(self, lk):
+        # a long launch is still running when the copy is attempted
+        from paper_1405_6162_b200.kernels import random_binary_state
+
+        shape = lk.LatticeShape(256, 128, 64)
+        f, g = random_binary_state(shape, np.random.default_rng(1))
+        dev = lk.TargetDevice()
+        lk.set_model_constants(dev, lk.D3Q19Model())
+        bf, bg = lk.target_malloc(dev, f.descriptor), lk.target_malloc(dev, g.descriptor)
+        lk.copy_to_target(bf, f)
+        lk.copy_to_target(bg, g)
+        plan = lk.LaunchPlan(extent=f.descriptor.padded_sites, vvl=1)
+        for _ in range(40):
+            lk.launch(dev, lk.binary_collision_kernel, plan, [bf, bg])
+        with pytest.raises((lk.ConcurrencyError, lk.LifecycleError)):
+            lk.copy_from_target(f, bf)
+            lk.target_free(bf)
+        lk.sync_target(dev)
+        lk.copy_from_target(f, bf)
+
+
+class TestBenchApi:
+    def test_benchmark_run_and_report(self, lk):
+        rows = lk.run_sweep("binary-collision", lk.LatticeShape(32, 32, 32), [1, 2, 4, 8], [1],
+                            ["cuda"], iterations=5)
+        assert len(rows) == 4 and all(r.sites_per_s > 0 for r in rows)
+        lines = lk.report_best(rows)
+        assert lines[0].startswith("binary-collision/cuda: best VVL=")
+        assert lk.emit_csv(rows).startswith("kernel,backend,nx,ny,nz,vvl,workers,tpb,iters")
