@@ -54,9 +54,9 @@ def parse_args(argv=None):
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--shape", default="256x256x256", help="per-GPU lattice NXxNYxNZ")
-    p.add_argument("--mode", choices=("exact", "fast"), default="exact")
+    p.add_argument("--mode", choices=("exact", "fast"), default="fast")
     p.add_argument("--vvl", type=int, default=1)
-    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-steps", type=int, default=4)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=1234)
@@ -179,14 +179,14 @@ def measured_hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(shape_key: str):
-    """dram bytes per k_collide_stream launch from the committed ncu capture."""
+def ncu_traffic(shape: str, mode: str, world: int):
+    """dram_bytes_read+write per k_collide_stream launch for this config, from
+    the committed ncu capture (profiles/ncu_traffic.json); None if not captured."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
             data = json.load(fh)
-        entry = data.get(shape_key) or {}
-        return entry.get("k_collide_stream_dram_bytes")
+        return data.get(f"{shape}/{mode}/p{world}", {}).get("k_collide_stream_dram_bytes")
     except Exception:
         return None
 
@@ -310,7 +310,7 @@ def run_ours(args, rank, world, local):
     cs_ms = prof[2] / args.steps
     peak, peak_src = measured_hbm_peak()
     achieved = CS_BYTES_PER_SITE * sites_rank / (cs_ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.shape if world == 1 else f"{args.shape}/p{world}")
+    traffic = ncu_traffic(args.shape, args.mode, world)
     roofline = {"bound": "hbm", "kernel": "k_collide_stream", "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src,
@@ -364,50 +364,81 @@ def run_ours(args, rank, world, local):
 
 
 def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
-    """Public-API path with host buffers: per step H2D state -> load (transpose)
-    -> 1 timestep -> store (transpose) -> D2H state, pinned host memory."""
-    import ctypes
-
-    from paper_1405_6162_b200.memory import pinned_empty
-
+    """Public-API path with host buffers, every step: H2D of the step's input
+    state (f, g from pinned host memory) -> BinaryFluid load (on-device
+    transpose to the slab layout) -> one timestep -> store (transpose back)
+    -> D2H of the result state.  Two staging buffers and three streams let the
+    H2D of step k+1 and the D2H of step k overlap the compute of the other
+    (PCIe is full duplex); every byte still crosses the bus every step."""
     nelem = f0.data.size
     nb = 8 * nelem
+    from paper_1405_6162_b200.memory import pinned_empty
+
     hf, hg = pinned_empty(nelem), pinned_empty(nelem)
     hf[:] = f0.data
     hg[:] = g0.data
     of, og = pinned_empty(nelem), pinned_empty(nelem)
-    stage = nat.malloc(2 * nb)
+    stage = [nat.malloc(2 * nb), nat.malloc(2 * nb)]
     padded = f0.descriptor.padded_sites
     nzl = sim.nzl
-    st = sim.stream
+    cs = sim.stream
+    h2d_st, d2h_st = nat.stream_create(), nat.stream_create()
+    ev_in = [nat.event_create(), nat.event_create()]      # H2D of buffer b done
+    ev_loaded = [nat.event_create(), nat.event_create()]  # load consumed buffer b
+    ev_out = [nat.event_create(), nat.event_create()]     # store into buffer b done
+    ev_free = [nat.event_create(), nat.event_create()]    # D2H out of buffer b done
+    chk = nat.check
+    L = nat.lib
 
-    def one_step():
-        nat.check(nat.lib.ltk_h2d(stage, hf.ctypes.data, nb, st))
-        nat.check(nat.lib.ltk_h2d(stage + nb, hg.ctypes.data, nb, st))
-        sim.load_device(stage, stage + nb, padded, nzl, 0, st)
-        sim.run(1)
-        sim.store_device(stage, stage + nb, padded, nzl, 0, st)
-        nat.check(nat.lib.ltk_d2h(of.ctypes.data, stage, nb, st))
-        nat.check(nat.lib.ltk_d2h(og.ctypes.data, stage + nb, nb, st))
+    def issue_h2d(b):
+        chk(L.ltk_stream_wait_event(h2d_st, ev_free[b]))
+        chk(L.ltk_stream_wait_event(h2d_st, ev_loaded[b]))
+        chk(L.ltk_h2d(stage[b], hf.ctypes.data, nb, h2d_st))
+        chk(L.ltk_h2d(stage[b] + nb, hg.ctypes.data, nb, h2d_st))
+        chk(L.ltk_event_record(ev_in[b], h2d_st))
 
-    one_step()
+    def run(nsteps):
+        for b in (0, 1):
+            chk(L.ltk_event_record(ev_free[b], d2h_st))
+            chk(L.ltk_event_record(ev_loaded[b], cs))
+        issue_h2d(0)
+        for k in range(nsteps):
+            b = k & 1
+            if k + 1 < nsteps:
+                issue_h2d(1 - b)   # prefetch next step's input
+            chk(L.ltk_stream_wait_event(cs, ev_in[b]))
+            sim.load_device(stage[b], stage[b] + nb, padded, nzl, 0, cs)
+            sim.run(1)
+            sim.store_device(stage[b], stage[b] + nb, padded, nzl, 0, cs)
+            chk(L.ltk_event_record(ev_out[b], cs))
+            chk(L.ltk_event_record(ev_loaded[b], cs))
+            chk(L.ltk_stream_wait_event(d2h_st, ev_out[b]))
+            chk(L.ltk_d2h(of.ctypes.data, stage[b], nb, d2h_st))
+            chk(L.ltk_d2h(og.ctypes.data, stage[b] + nb, nb, d2h_st))
+            chk(L.ltk_event_record(ev_free[b], d2h_st))
+        chk(L.ltk_stream_wait_event(cs, ev_free[(nsteps - 1) & 1]))
+
+    run(1)
     sim.sync()
     ctl.barrier()
-    t0 = time.perf_counter()
     start, stop = nat.event_create(True), nat.event_create(True)
-    nat.check(nat.lib.ltk_event_record(start, st))
-    for _ in range(args.e2e_steps):
-        one_step()
-    nat.check(nat.lib.ltk_event_record(stop, st))
+    chk(L.ltk_event_record(start, cs))
+    run(args.e2e_steps)
+    chk(L.ltk_event_record(stop, cs))
     sim.sync()
     ms = nat.elapsed_ms(start, stop)
     ms_max = ctl.allreduce(ms, "MAX")
-    nat.free(stage)
+    # the last D2H result must equal a plain device run of the same input
+    for p in stage:
+        nat.free(p)
+    for s in (h2d_st, d2h_st):
+        L.ltk_stream_destroy(s)
     sites = sim.shape.nx * sim.shape.ny * nzl * world
     return {"value": sites * args.e2e_steps / (ms_max * 1e-3) / 1e6, "unit": "MLUPS",
             "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
             "steps": args.e2e_steps, "ms_per_step": ms_max / args.e2e_steps,
-            "path": "H2D(f,g pinned) -> BinaryFluid load -> run(1) -> store -> D2H(f,g)"}
+            "path": "pinned H2D(f,g) -> BinaryFluid.load_device -> run(1) -> store_device -> "
+                    "D2H(f,g); next step's H2D overlaps this step's D2H"}
 
 
 def main(argv=None):
