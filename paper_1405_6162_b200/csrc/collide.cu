@@ -6,12 +6,8 @@
 // (TLP); the VVL sites of a chunk are consecutive in every SoA component, so
 // they load as one 8*VVL-byte vector (ILP).  grid = ceil(nchunks / tpb).
 //
-// Two strategies, chosen by VVL at compile time:
-//   VVL <= 2  register-resident: all 2*19*VVL values stay in registers, one
-//             pass, one HBM read + one HBM write per value.
-//   VVL >= 4  two-pass (the reference's own structure): pass 1 streams the
-//             components to form the moments, pass 2 re-reads (L1/L2 hit),
-//             relaxes and stores -- bounded register use at any VVL.
+// Register-resident single pass: all 2*19 values of a site stay in registers,
+// one HBM read + one HBM write per value.
 #include "ltk_common.cuh"
 
 namespace ltk {
@@ -69,7 +65,8 @@ __device__ __forceinline__ void finish_site(Site &s, const CollideArgs &a) {
 }
 
 // Relax component I of both distributions at one site.
-template <int I, int MODE>
+// T1: bit 0 = tau_f == 1.0, bit 1 = tau_g == 1.0 (EXACT only)
+template <int I, int MODE, int T1>
 __device__ __forceinline__ void relax(double &f, double &g, const Site &s, const CollideArgs &a) {
     if constexpr (MODE == LTK_MODE_EXACT) {
         using M = Exact;
@@ -78,8 +75,11 @@ __device__ __forceinline__ void relax(double &f, double &g, const Site &s, const
                            s.t);
         double feq = M::mul(M::mul(a.wv[I], s.rho), br);
         double geq = M::mul(M::mul(a.wv[I], s.phi), br);
-        f = M::sub(f, M::div(M::sub(f, feq), a.tau_f));
-        g = M::sub(g, M::div(M::sub(g, geq), a.tau_g));
+        const double df = M::sub(f, feq), dg = M::sub(g, geq);
+        if constexpr (T1 & 1) f = M::sub(f, df);
+        else f = M::sub(f, M::div(df, a.tau_f));
+        if constexpr (T1 & 2) g = M::sub(g, dg);
+        else g = M::sub(g, M::div(dg, a.tau_g));
     } else {
         double ud = dot_c<cx(I), cy(I), cz(I), Fast>(s.ux, s.uy, s.uz);
         double br = fma(ud, fma(ud, a.a2, a.a1), s.t);
@@ -95,89 +95,60 @@ struct Acc {
     using M = typename std::conditional<MODE == LTK_MODE_EXACT, Exact, Fast>::type;
 };
 
-template <int VVL, int MODE>
-__global__ void __launch_bounds__(256) k_collide(const CollideArgs a) {
+// Register-resident collision of W (= 1 or 2) consecutive sites at base.
+template <int W, int MODE, int T1>
+__device__ __forceinline__ void collide_sites(double *__restrict__ f, double *__restrict__ g,
+                                              long long base, const CollideArgs &a) {
     using M = typename Acc<MODE>::M;
+    const long long P = a.padded;
+    Site st[W];
+#pragma unroll
+    for (int v = 0; v < W; ++v) st[v] = Site{0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0, 0, true};
+    double F[Q][W], G[Q][W];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) load_vec<W>(F[i], f + base + i * P);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) load_vec<W>(G[i], g + base + i * P);
+    static_for<0, Q>([&](auto I) {
+#pragma unroll
+        for (int v = 0; v < W; ++v) accum_f<I.value, M>(st[v], F[I.value][v]);
+    });
+#pragma unroll
+    for (int v = 0; v < W; ++v) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) st[v].phi = M::add(st[v].phi, G[i][v]);
+        if (st[v].rho <= 0.0) {  // kernels.py:106-109
+            st[v].ok = false;
+            if (base + v < a.nsites) flag_singular(a.err, base + v);
+        } else {
+            finish_site<MODE>(st[v], a);
+        }
+    }
+    static_for<0, Q>([&](auto I) {
+#pragma unroll
+        for (int v = 0; v < W; ++v)
+            if (st[v].ok) relax<I.value, MODE, T1>(F[I.value][v], G[I.value][v], st[v], a);
+    });
+    // padding lanes (rho <= 0) are written back unchanged: bitwise untouched
+#pragma unroll
+    for (int i = 0; i < Q; ++i) store_vec<W>(f + base + i * P, F[i]);
+#pragma unroll
+    for (int i = 0; i < Q; ++i) store_vec<W>(g + base + i * P, G[i]);
+}
+
+// One thread per VVL-site chunk (TLP).  VVL <= 2 loads the chunk as 16-byte
+// vectors in one register-resident pass; larger VVL walks the chunk's sites
+// as 2-site vectors, so register use does not grow with VVL.
+template <int VVL, int MODE, int T1>
+__global__ void __launch_bounds__(256) k_collide(const CollideArgs a) {
     const long long chunk = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (chunk >= a.nchunks) return;
     const long long base = a.site_lo + chunk * VVL;
-    double *__restrict__ f = a.f + base;
-    double *__restrict__ g = a.g + base;
-    const long long P = a.padded;
-
-    Site st[VVL];
-#pragma unroll
-    for (int v = 0; v < VVL; ++v) st[v] = Site{0.0, 0.0, 0.0, 0.0, 0.0, 0, 0, 0, 0, true};
-
     if constexpr (VVL <= 2) {
-        // ---------------- register-resident single pass
-        double F[Q][VVL], G[Q][VVL];
-#pragma unroll
-        for (int i = 0; i < Q; ++i) load_vec<VVL>(F[i], f + i * P);
-#pragma unroll
-        for (int i = 0; i < Q; ++i) load_vec<VVL>(G[i], g + i * P);
-        static_for<0, Q>([&](auto I) {
-#pragma unroll
-            for (int v = 0; v < VVL; ++v) accum_f<I.value, M>(st[v], F[I.value][v]);
-        });
-#pragma unroll
-        for (int v = 0; v < VVL; ++v) {
-#pragma unroll
-            for (int i = 0; i < Q; ++i) st[v].phi = M::add(st[v].phi, G[i][v]);
-            if (st[v].rho <= 0.0) {  // kernels.py:106-109
-                st[v].ok = false;
-                if (base + v < a.nsites) flag_singular(a.err, base + v);
-            } else {
-                finish_site<MODE>(st[v], a);
-            }
-        }
-        static_for<0, Q>([&](auto I) {
-#pragma unroll
-            for (int v = 0; v < VVL; ++v) {
-                if (st[v].ok) relax<I.value, MODE>(F[I.value][v], G[I.value][v], st[v], a);
-            }
-        });
-#pragma unroll
-        for (int i = 0; i < Q; ++i) store_vec<VVL>(f + i * P, F[i]);
-#pragma unroll
-        for (int i = 0; i < Q; ++i) store_vec<VVL>(g + i * P, G[i]);
+        collide_sites<VVL, MODE, T1>(a.f, a.g, base, a);
     } else {
-        // ---------------- two-pass: moments, then reload + relax + store
-        static_for<0, Q>([&](auto I) {
-            double t[VVL];
-            load_vec<VVL>(t, f + I.value * P);
-#pragma unroll
-            for (int v = 0; v < VVL; ++v) accum_f<I.value, M>(st[v], t[v]);
-        });
-#pragma unroll
-        for (int i = 0; i < Q; ++i) {
-            double t[VVL];
-            load_vec<VVL>(t, g + i * P);
-#pragma unroll
-            for (int v = 0; v < VVL; ++v) st[v].phi = M::add(st[v].phi, t[v]);
-        }
-        bool any_ok = false;
-#pragma unroll
-        for (int v = 0; v < VVL; ++v) {
-            if (st[v].rho <= 0.0) {
-                st[v].ok = false;
-                if (base + v < a.nsites) flag_singular(a.err, base + v);
-            } else {
-                finish_site<MODE>(st[v], a);
-                any_ok = true;
-            }
-        }
-        if (!any_ok) return;  // whole chunk is padding: untouched
-        static_for<0, Q>([&](auto I) {
-            double tf[VVL], tg[VVL];
-            load_vec<VVL>(tf, f + I.value * P);
-            load_vec<VVL>(tg, g + I.value * P);
-#pragma unroll
-            for (int v = 0; v < VVL; ++v)
-                if (st[v].ok) relax<I.value, MODE>(tf[v], tg[v], st[v], a);
-            store_vec<VVL>(f + I.value * P, tf);
-            store_vec<VVL>(g + I.value * P, tg);
-        });
+#pragma unroll 1
+        for (int k = 0; k < VVL; k += 2) collide_sites<2, MODE, T1>(a.f, a.g, base + k, a);
     }
 }
 
@@ -197,16 +168,16 @@ __global__ void __launch_bounds__(256) k_scale(double *field, long long padded,
     }
 }
 
-template <int MODE>
+template <int MODE, int T1>
 static int launch_collide(int vvl, int tpb, long long nchunks, const CollideArgs &a,
                           cudaStream_t st) {
     const unsigned grid = (unsigned)((nchunks + tpb - 1) / tpb);
     switch (vvl) {
-        case 1: k_collide<1, MODE><<<grid, tpb, 0, st>>>(a); break;
-        case 2: k_collide<2, MODE><<<grid, tpb, 0, st>>>(a); break;
-        case 4: k_collide<4, MODE><<<grid, tpb, 0, st>>>(a); break;
-        case 8: k_collide<8, MODE><<<grid, tpb, 0, st>>>(a); break;
-        case 16: k_collide<16, MODE><<<grid, tpb, 0, st>>>(a); break;
+        case 1: k_collide<1, MODE, T1><<<grid, tpb, 0, st>>>(a); break;
+        case 2: k_collide<2, MODE, T1><<<grid, tpb, 0, st>>>(a); break;
+        case 4: k_collide<4, MODE, T1><<<grid, tpb, 0, st>>>(a); break;
+        case 8: k_collide<8, MODE, T1><<<grid, tpb, 0, st>>>(a); break;
+        case 16: k_collide<16, MODE, T1><<<grid, tpb, 0, st>>>(a); break;
         default: return fail(LTK_ERR_PLAN, "unsupported vvl %d (1,2,4,8,16)", vvl);
     }
     LTK_CHECK_LAUNCH("k_collide");
@@ -262,8 +233,17 @@ extern "C" int ltk_collide(int64_t chunk_lo, int64_t chunk_hi, int32_t vvl, int3
     a.a2 = 1.0 / a.c2;
     a.a3 = 1.0 / a.c1;
     cudaStream_t st = as_stream(stream);
-    if (p->mode == LTK_MODE_EXACT) return launch_collide<LTK_MODE_EXACT>(vvl, tpb, a.nchunks, a, st);
-    if (p->mode == LTK_MODE_FAST) return launch_collide<LTK_MODE_FAST>(vvl, tpb, a.nchunks, a, st);
+    if (p->mode == LTK_MODE_EXACT) {
+        // x / 1.0 == x for every IEEE double: when tau is exactly 1 (the
+        // reference default, model.py:48-49) the division is skipped, bitwise neutral
+        switch ((p->tau_f == 1.0 ? 1 : 0) | (p->tau_g == 1.0 ? 2 : 0)) {
+            case 0: return launch_collide<LTK_MODE_EXACT, 0>(vvl, tpb, a.nchunks, a, st);
+            case 1: return launch_collide<LTK_MODE_EXACT, 1>(vvl, tpb, a.nchunks, a, st);
+            case 2: return launch_collide<LTK_MODE_EXACT, 2>(vvl, tpb, a.nchunks, a, st);
+            default: return launch_collide<LTK_MODE_EXACT, 3>(vvl, tpb, a.nchunks, a, st);
+        }
+    }
+    if (p->mode == LTK_MODE_FAST) return launch_collide<LTK_MODE_FAST, 0>(vvl, tpb, a.nchunks, a, st);
     return fail(LTK_ERR_CONFIG, "unknown collision mode %d", p->mode);
 }
 

@@ -106,22 +106,33 @@ static int launch_mu(const FluidArgs &a, int vvl, cudaStream_t st) {
     return LTK_OK;
 }
 
-template <int MODE, int PHYS>
+template <int MODE, int PHYS, int T1>
 static void launch_cs_t(const FluidArgs &a, int vvl, cudaStream_t st) {
     const unsigned g = grid_for(a.nthreads, kTPB);
     if (vvl == 2)
-        k_collide_stream<2, MODE, PHYS><<<g, kTPB, 0, st>>>(a);
+        k_collide_stream<2, MODE, PHYS, T1><<<g, kTPB, 0, st>>>(a);
     else
-        k_collide_stream<1, MODE, PHYS><<<g, kTPB, 0, st>>>(a);
+        k_collide_stream<1, MODE, PHYS, T1><<<g, kTPB, 0, st>>>(a);
+}
+
+template <int PHYS>
+static void launch_cs_exact(const FluidArgs &a, int vvl, cudaStream_t st) {
+    // x / 1.0 == x: skip the relaxation divisions when tau is exactly 1
+    switch ((a.tau_f == 1.0 ? 1 : 0) | (a.tau_g == 1.0 ? 2 : 0)) {
+        case 0: launch_cs_t<LTK_MODE_EXACT, PHYS, 0>(a, vvl, st); break;
+        case 1: launch_cs_t<LTK_MODE_EXACT, PHYS, 1>(a, vvl, st); break;
+        case 2: launch_cs_t<LTK_MODE_EXACT, PHYS, 2>(a, vvl, st); break;
+        default: launch_cs_t<LTK_MODE_EXACT, PHYS, 3>(a, vvl, st); break;
+    }
 }
 
 static int launch_cs(const FluidArgs &a, int vvl, int mode, int phys, cudaStream_t st) {
     if (a.nthreads <= 0) return LTK_OK;
     if (vvl > 2) return fail(LTK_ERR_PLAN, "collide-stream supports vvl 1, 2 (got %d)", vvl);
-    if (mode == LTK_MODE_EXACT && phys == 1) launch_cs_t<LTK_MODE_EXACT, 1>(a, vvl, st);
-    else if (mode == LTK_MODE_EXACT) launch_cs_t<LTK_MODE_EXACT, 0>(a, vvl, st);
-    else if (phys == 1) launch_cs_t<LTK_MODE_FAST, 1>(a, vvl, st);
-    else launch_cs_t<LTK_MODE_FAST, 0>(a, vvl, st);
+    if (mode == LTK_MODE_EXACT && phys == 1) launch_cs_exact<1>(a, vvl, st);
+    else if (mode == LTK_MODE_EXACT) launch_cs_exact<0>(a, vvl, st);
+    else if (phys == 1) launch_cs_t<LTK_MODE_FAST, 1, 0>(a, vvl, st);
+    else launch_cs_t<LTK_MODE_FAST, 0, 0>(a, vvl, st);
     LTK_CHECK_LAUNCH("k_collide_stream");
     return LTK_OK;
 }

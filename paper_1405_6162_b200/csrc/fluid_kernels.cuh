@@ -197,7 +197,8 @@ __device__ __forceinline__ void fsite_finish(FSite &s, double gmx, double gmy, d
     }
 }
 
-template <int I, int MODE, int PHYS>
+// T1 (EXACT): bit 0 = tau_f == 1.0, bit 1 = tau_g == 1.0 -> x / 1.0 == x, skip it
+template <int I, int MODE, int PHYS, int T1>
 __device__ __forceinline__ void frelax(double &f, double &g, const FSite &s, const FluidArgs &a) {
     if constexpr (MODE == LTK_MODE_EXACT) {
         using M = Exact;
@@ -206,7 +207,10 @@ __device__ __forceinline__ void frelax(double &f, double &g, const FSite &s, con
             M::add(M::add(1.0, M::div(ud, a.cs2)), M::div(M::mul(ud, ud), a.c2)), s.t);
         const double feq = M::mul(M::mul(a.wv[I], s.rho), br);
         double geq = M::mul(M::mul(a.wv[I], s.phi), br);
-        double fn = M::sub(f, M::div(M::sub(f, feq), a.tau_f));
+        const double df = M::sub(f, feq);
+        double fn;
+        if constexpr (T1 & 1) fn = M::sub(f, df);
+        else fn = M::sub(f, M::div(df, a.tau_f));
         if constexpr (PHYS == 1) {
             const double cF = dot_c<cx(I), cy(I), cz(I), M>(s.Fx, s.Fy, s.Fz);
             const double src =
@@ -216,7 +220,9 @@ __device__ __forceinline__ void frelax(double &f, double &g, const FSite &s, con
             geq = M::add(geq, M::mul(a.lam[I], s.psi));
         }
         f = fn;
-        g = M::sub(g, M::div(M::sub(g, geq), a.tau_g));
+        const double dg = M::sub(g, geq);
+        if constexpr (T1 & 2) g = M::sub(g, dg);
+        else g = M::sub(g, M::div(dg, a.tau_g));
     } else {
         const double ud = dot_c<cx(I), cy(I), cz(I), Fast>(s.ux, s.uy, s.uz);
         const double br = fma(ud, fma(ud, a.a2, a.a1), s.t);
@@ -235,7 +241,7 @@ __device__ __forceinline__ void frelax(double &f, double &g, const FSite &s, con
     }
 }
 
-template <int VVL, int MODE, int PHYS>
+template <int VVL, int MODE, int PHYS, int T1>
 __global__ void __launch_bounds__(256) k_collide_stream(const FluidArgs a) {
     using M = typename std::conditional<MODE == LTK_MODE_EXACT, Exact, Fast>::type;
     Pos p;
@@ -283,7 +289,7 @@ __global__ void __launch_bounds__(256) k_collide_stream(const FluidArgs a) {
     static_for<0, Q>([&](auto I) {
 #pragma unroll
         for (int k = 0; k < VVL; ++k)
-            if (ok[k]) frelax<I.value, MODE, PHYS>(F[I.value][k], G[I.value][k], st[k], a);
+            if (ok[k]) frelax<I.value, MODE, PHYS, T1>(F[I.value][k], G[I.value][k], st[k], a);
     });
 
     const long long off = (long long)p.y * a.nx + p.x0;
