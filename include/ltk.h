@@ -146,12 +146,10 @@ int ltk_unpack_sites(double *dst, const double *packed, const int64_t *idx, int6
 /* ------------------------------------------------------------ full timestep
  * Builder-defined extension.
  *
- * Device layout of a slab: distributions are SoA with
- * component stride `cstride` doubles; inside a component, storage plane
- * zs = z + 1 (z = 0..nzl-1 owned, zs = 0 and zs = nzl+1 are halo planes), site
- * (x, y) at zs*nx*ny + y*nx + x (x fastest).  Scalar fields (phi, mu) have
- * halo depth 2: nzl + 4 planes, owned plane z at zs = z + 2.  Periodic in x
- * and y; z neighbours come from the halo planes.
+ * Device layout of a slab: SoA, component stride `cstride`
+ * doubles; inside a component, storage plane zs = z + 1 (z = 0..nzl-1 owned,
+ * zs = 0 and zs = nzl+1 are halo planes), site (x, y) at zs*nx*ny + y*nx + x
+ * (x fastest).  Periodic in x and y; z neighbours come from the halo planes.
  */
 typedef struct {
     double wv[LTK_Q];
@@ -170,19 +168,16 @@ typedef struct {
 /* phi(x) = sum_i g_i(x - c_i) on owned planes [z_lo, z_hi) (pull). */
 int ltk_fluid_phi(const ltk_slab *s, const double *g, double *phi, int64_t z_lo,
                   int64_t z_hi, void *stream);
-/* Observable mu = A phi + B phi^3 - kappa lap7(phi) on owned planes [z_lo, z_hi)
- * (needs phi halos of depth >= 1; the collision evaluates mu itself). */
+/* mu = A phi + B phi^3 - kappa lap7(phi) on owned planes [z_lo, z_hi). */
 int ltk_fluid_mu(const ltk_slab *s, const double *phi, double *mu,
                  const ltk_fluid_params *p, int64_t z_lo, int64_t z_hi, void *stream);
-/* Pull-stream + collide owned planes [z_lo, z_hi): f_out(x) = C(f_in(x-c_i), ...);
- * mu and grad mu are evaluated from phi (needs phi halos of depth 2). */
+/* Pull-stream + collide owned planes [z_lo, z_hi): f_out(x) = C(f_in(x-c_i), ...). */
 int ltk_fluid_collide_stream(const ltk_slab *s, const double *f_in, const double *g_in,
-                             const double *phi, double *f_out, double *g_out,
+                             const double *mu, double *f_out, double *g_out,
                              const ltk_fluid_params *p, int64_t z_lo, int64_t z_hi,
                              int32_t vvl, void *stream);
 /* Periodic z wrap on one device: copy owned boundary planes into the halo
- * planes.  which: bit0 = f/g crossing components (depth 1), bit1 = phi,
- * bit2 = mu (depth 2). */
+ * planes.  which: bit0 = f/g crossing components, bit1 = phi, bit2 = mu. */
 int ltk_fluid_wrap_halos(const ltk_slab *s, double *f, double *g, double *phi, double *mu,
                          int32_t which, void *stream);
 /* Halo faces of the distributions: pack the 5 f + 5 g components that cross

@@ -334,6 +334,7 @@ static FluidArgs engine_args(const ltk_fluid *e, int in_state) {
     a.g_out = e->fg[1 - in_state][1];
     a.phi_in = e->phi;
     a.phi_out = e->phi;
+    a.mu = e->mu;
     a.mu_out = e->mu;
     a.err = singular_word();
     a.wrap = (e->nranks == 1 && e->comm == nullptr) ? 1 : 0;
@@ -341,7 +342,7 @@ static FluidArgs engine_args(const ltk_fluid *e, int in_state) {
 }
 
 // One NCCL halo exchange group on comm_st.  kind 0: f/g crossing components
-// of state `s` (depth 1); kind 1: phi (depth 2).  Send order per peer is fixed
+// of state `s`; kind 1: phi; kind 2: mu.  Send order per peer is fixed
 // (faces up, then faces down) and receive order mirrors it, which keeps the
 // matching right even when both neighbours are the same rank (P = 2) or
 // this rank itself (P = 1).
@@ -349,7 +350,7 @@ static int exchange(ltk_fluid *e, int kind, int s) {
     Nccl &n = nccl();
     const int up = (e->rank + 1) % e->nranks, down = (e->rank + e->nranks - 1) % e->nranks;
     const size_t PL = (size_t)(e->nx * e->ny);
-    const long long top = e->nzl, bot = 1, halo_lo = 0, halo_hi = e->nzl + 1;  // f/g planes
+    const long long top = e->nzl, bot = 1, halo_lo = 0, halo_hi = e->nzl + 1;
     const ltk_slab *sl = &e->slab;
     LTK_NCCL(n.GroupStart());
     if (kind == 0) {
@@ -370,18 +371,11 @@ static int exchange(ltk_fluid *e, int kind, int s) {
                 LTK_NCCL(n.Recv(plane(e->fg[s][d], sl, kDown[j], halo_hi), PL, ncclFloat64, up,
                                 e->comm, e->comm_st));
     } else {
-        // phi, halo depth 2: owned planes nzl-2, nzl-1 (zs = nzl, nzl+1) go up,
-        // owned planes 0, 1 (zs = 2, 3) go down; receive into zs = 0, 1 from
-        // below and zs = nzl+2, nzl+3 from above
-        double *b = e->phi;
-        for (int k = 0; k < 2; ++k)
-            LTK_NCCL(n.Send(b + (e->nzl + k) * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
-        for (int k = 0; k < 2; ++k)
-            LTK_NCCL(n.Send(b + (2 + k) * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
-        for (int k = 0; k < 2; ++k)
-            LTK_NCCL(n.Recv(b + k * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
-        for (int k = 0; k < 2; ++k)
-            LTK_NCCL(n.Recv(b + (e->nzl + 2 + k) * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
+        double *b = kind == 1 ? e->phi : e->mu;
+        LTK_NCCL(n.Send(b + top * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
+        LTK_NCCL(n.Send(b + bot * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
+        LTK_NCCL(n.Recv(b + halo_lo * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
+        LTK_NCCL(n.Recv(b + halo_hi * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
     }
     LTK_NCCL(n.GroupEnd());
     return LTK_OK;
@@ -394,62 +388,76 @@ static int exchange(ltk_fluid *e, int kind, int s) {
     } while (0)
 
 // Enqueue one timestep reading state `s` and writing state 1 - s.
-// Profile slots: [0,1) phi (+ f/g halo wait), [1,2) collide-stream interior,
-// [2,3) collide-stream boundary (+ phi halo wait); one slab: [1,2) is empty.
 static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
     FluidArgs a = engine_args(e, s);
     const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
     const long long nzl = e->nzl;
     if (prof) cudaEventRecord(e->pev[0], st);
     if (e->comm == nullptr) {
-        // single slab, periodic z: two kernels, halos written by the kernels
+        // single slab, periodic z: three kernels, halos written by the kernels
         set_planes(a, vvl, 0, nzl);
         LTK_RC(launch_phi(a, vvl, st));
         if (prof) cudaEventRecord(e->pev[1], st);
+        if (phys == 1) LTK_RC(launch_mu(a, vvl, st));
         if (prof) cudaEventRecord(e->pev[2], st);
         LTK_RC(launch_cs(a, vvl, mode, phys, st));
         if (prof) cudaEventRecord(e->pev[3], st);
         return LTK_OK;
     }
-    // z-slabs: each exchange overlaps the interior planes of the next kernel.
-    // phi interior = [1, nzl-1) (pull radius 1); collide interior = [2, nzl-2)
-    // (mu needs phi at distance 2).
-    auto ranges = [&](long long lo, long long hi, auto launch_one) -> int {
-        if (hi > lo) {
-            set_planes(a, vvl, lo, hi);
-            return launch_one();
+    // z-slabs: each exchange overlaps the interior planes of the next kernel
+    const long long in_lo = 1, in_hi = nzl - 1;  // interior (may be empty)
+    auto boundary = [&](auto launch_one) -> int {
+        set_planes(a, vvl, 0, 1);
+        LTK_RC(launch_one());
+        if (nzl > 1) {
+            set_planes(a, vvl, nzl - 1, nzl);
+            LTK_RC(launch_one());
         }
         return LTK_OK;
     };
-    auto launch_p = [&] { return launch_phi(a, vvl, st); };
-    auto launch_c = [&] { return launch_cs(a, vvl, mode, phys, st); };
-    // (1) f/g faces || phi interior, then the phi boundary planes
+    // (1) f/g faces || phi interior
     LTK_CUDA(cudaEventRecord(e->ev_fork[0], st));
     LTK_CUDA(cudaStreamWaitEvent(e->comm_st, e->ev_fork[0], 0));
     LTK_RC(exchange(e, 0, s));
     LTK_CUDA(cudaEventRecord(e->ev_join[0], e->comm_st));
-    LTK_RC(ranges(1, nzl - 1, launch_p));
+    if (in_hi > in_lo) {
+        set_planes(a, vvl, in_lo, in_hi);
+        LTK_RC(launch_phi(a, vvl, st));
+    }
     LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[0], 0));
-    LTK_RC(ranges(0, 1, launch_p));
-    if (nzl > 1) LTK_RC(ranges(nzl - 1, nzl, launch_p));
+    LTK_RC(boundary([&] { return launch_phi(a, vvl, st); }));
     if (prof) cudaEventRecord(e->pev[1], st);
-    // (2) phi faces (depth 2) || collide-stream interior, then its boundary planes
-    LTK_CUDA(cudaEventRecord(e->ev_fork[1], st));
-    LTK_CUDA(cudaStreamWaitEvent(e->comm_st, e->ev_fork[1], 0));
-    LTK_RC(exchange(e, 1, s));
-    LTK_CUDA(cudaEventRecord(e->ev_join[1], e->comm_st));
-    const long long lo2 = std::min<long long>(2, nzl), hi2 = std::max<long long>(nzl - 2, lo2);
-    LTK_RC(ranges(lo2, hi2, launch_c));
+    if (phys == 1) {
+        // (2) phi faces || mu interior
+        LTK_CUDA(cudaEventRecord(e->ev_fork[1], st));
+        LTK_CUDA(cudaStreamWaitEvent(e->comm_st, e->ev_fork[1], 0));
+        LTK_RC(exchange(e, 1, s));
+        LTK_CUDA(cudaEventRecord(e->ev_join[1], e->comm_st));
+        if (in_hi > in_lo) {
+            set_planes(a, vvl, in_lo, in_hi);
+            LTK_RC(launch_mu(a, vvl, st));
+        }
+        LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[1], 0));
+        LTK_RC(boundary([&] { return launch_mu(a, vvl, st); }));
+        // (3) mu faces || collide-stream interior
+        LTK_CUDA(cudaEventRecord(e->ev_fork[2], st));
+        LTK_CUDA(cudaStreamWaitEvent(e->comm_st, e->ev_fork[2], 0));
+        LTK_RC(exchange(e, 2, s));
+        LTK_CUDA(cudaEventRecord(e->ev_join[2], e->comm_st));
+    }
     if (prof) cudaEventRecord(e->pev[2], st);
-    LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[1], 0));
-    LTK_RC(ranges(0, lo2, launch_c));
-    LTK_RC(ranges(hi2, nzl, launch_c));
+    if (in_hi > in_lo) {
+        set_planes(a, vvl, in_lo, in_hi);
+        LTK_RC(launch_cs(a, vvl, mode, phys, st));
+    }
+    if (phys == 1) LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[2], 0));
+    LTK_RC(boundary([&] { return launch_cs(a, vvl, mode, phys, st); }));
     if (prof) cudaEventRecord(e->pev[3], st);
     return LTK_OK;
 }
 
 static int wrap_state_halos(ltk_fluid *e, int s, int which, cudaStream_t st) {
-    return ltk_fluid_wrap_halos(&e->slab, e->fg[s][0], e->fg[s][1], e->phi, nullptr, which, st);
+    return ltk_fluid_wrap_halos(&e->slab, e->fg[s][0], e->fg[s][1], e->phi, e->mu, which, st);
 }
 
 }  // namespace ltk
@@ -483,7 +491,7 @@ int ltk_fluid_mu(const ltk_slab *s, const double *phi, double *mu, const ltk_flu
 }
 
 int ltk_fluid_collide_stream(const ltk_slab *s, const double *f_in, const double *g_in,
-                             const double *phi, double *f_out, double *g_out,
+                             const double *mu, double *f_out, double *g_out,
                              const ltk_fluid_params *p, int64_t z_lo, int64_t z_hi, int32_t vvl,
                              void *stream) {
     LTK_RC(check_slab(s, vvl));
@@ -493,7 +501,7 @@ int ltk_fluid_collide_stream(const ltk_slab *s, const double *f_in, const double
     fill_args(a, s, p);
     a.f_in = f_in;
     a.g_in = g_in;
-    a.phi_in = phi;
+    a.mu = mu;
     a.f_out = f_out;
     a.g_out = g_out;
     a.err = singular_word();
@@ -521,13 +529,10 @@ int ltk_fluid_wrap_halos(const ltk_slab *s, double *f, double *g, double *phi, d
     for (int k = 0; k < 2; ++k) {
         double *b = k == 0 ? phi : mu;
         if (!(which & (2 << k)) || !b) continue;
-        // scalar fields: halo depth 2, halo plane hz holds owned plane (hz - 2) mod nzl
-        const long long hz[4] = {0, 1, nzl + 2, nzl + 3};
-        for (long long h : hz) {
-            long long src = ((h - kSOff) % nzl + nzl) % nzl;
-            pc.src[pc.n] = b + (src + kSOff) * pc.PL;
-            pc.dst[pc.n++] = b + h * pc.PL;
-        }
+        pc.src[pc.n] = b + nzl * pc.PL;
+        pc.dst[pc.n++] = b;
+        pc.src[pc.n] = b + pc.PL;
+        pc.dst[pc.n++] = b + (nzl + 1) * pc.PL;
     }
     return run_plane_copies(pc, as_stream(stream));
 }
@@ -637,15 +642,13 @@ int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank, in
     e->slab.cstride = (raw + 63) / 64 * 64;
     int rc = check_slab(&e->slab, vvl);
     if (!rc && vvl > 2) rc = fail(LTK_ERR_PLAN, "engine vvl must be 1 or 2");
-    if (!rc && nranks > 1 && e->nzl < 2)
-        rc = fail(LTK_ERR_SHAPE, "z-slabs need >= 2 planes per rank (phi halo depth 2)");
     if (rc) {
         delete e;
         return rc;
     }
     cudaGetDevice(&e->dev);
     const size_t dist_bytes = (size_t)e->slab.cstride * Q * sizeof(double);
-    const size_t plane_bytes = (size_t)(e->nzl + 2 * kSOff) * nx * ny * sizeof(double);
+    const size_t plane_bytes = (size_t)raw * sizeof(double);
     void *ptr = nullptr;
     for (int s = 0; s < 2; ++s)
         for (int d = 0; d < 2; ++d) {

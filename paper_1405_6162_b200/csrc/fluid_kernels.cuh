@@ -7,19 +7,14 @@
 // is one contiguous run of PL doubles per component (halo faces are plain
 // contiguous NCCL buffers) and a warp touches 32 consecutive x.
 //
-// Scalar fields (phi, mu) use halo depth 2: storage plane zs = z + 2 of
-// nzl + 4 planes (kSOff), because the collision evaluates mu itself from a
-// radius-2 phi stencil.
-//
-// One timestep = k_phi -> k_collide_stream (pull scheme):
+// One timestep = k_phi -> k_mu -> k_collide_stream (pull scheme):
 //   k_phi   phi(x) = sum_i g_i(x - c_i)                         [g pulled]
-//   k_cs    pull f, g; phi again in registers; mu at x and its 6 neighbours
-//           from phi (7-point Laplacian, mu_at); grad mu (central);
+//   k_mu    mu = A phi + B phi^3 - kappa lap7(phi)               [phi stencil]
+//   k_cs    pull f, g; phi again in registers; grad mu (central);
 //           Guo-forced BGK for f, chemical-potential g_eq; aligned store.
-// k_mu (the same mu_at, bitwise) only serves observables.
 // With `wrap` set (single slab, periodic z) each kernel also writes the
-// periodic images of its boundary planes into the halo planes, so a one-GPU
-// step needs no halo kernels at all.
+// periodic image of its boundary plane into the opposite halo plane, so a
+// one-GPU step needs no halo kernels at all.
 #pragma once
 
 #include "ltk_common.cuh"
@@ -29,6 +24,7 @@ namespace ltk {
 struct FluidArgs {
     const double *f_in;
     const double *g_in;
+    const double *mu;
     const double *phi_in;
     double *f_out;
     double *g_out;
@@ -47,8 +43,6 @@ struct FluidArgs {
     double c1, c2, cs2sq, srcpre;                 // 2cs2, (2cs2)cs2, cs2*cs2, 1 - 0.5/tau_f
     double inv_tau_f, inv_tau_g, a1, a2, a3, inv_cs2, inv_cs2sq;  // FAST
 };
-
-constexpr int kSOff = 2;  // storage plane of owned scalar plane z is z + kSOff
 
 // thread -> (x0, y, z) of a VVL-site row segment
 struct Pos {
@@ -101,49 +95,45 @@ __global__ void __launch_bounds__(256) k_phi(const FluidArgs a) {
         for (int k = 0; k < VVL; ++k) phi[k] = __dadd_rn(phi[k], v[k]);
     });
     const long long off = (long long)p.y * a.nx + p.x0;
-    store_vec<VVL>(a.phi_out + (long long)(p.z + kSOff) * a.PL + off, phi);
-    if (a.wrap) {
-        // periodic images: halo planes zs = 0, 1, nzl+2, nzl+3 hold owned
-        // planes (zs - 2) mod nzl
-        const int hz[4] = {0, 1, a.nzl + 2, a.nzl + 3};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            int src = (hz[h] - kSOff) % a.nzl;
-            if (src < 0) src += a.nzl;
-            if (src == p.z) store_vec<VVL>(a.phi_out + (long long)hz[h] * a.PL + off, phi);
-        }
+    store_vec<VVL>(a.phi_out + (long long)(p.z + 1) * a.PL + off, phi);
+    if (a.wrap) {  // periodic images for the mu stencil
+        if (p.z == 0) store_vec<VVL>(a.phi_out + (long long)(a.nzl + 1) * a.PL + off, phi);
+        if (p.z == a.nzl - 1) store_vec<VVL>(a.phi_out + off, phi);
     }
 }
 
 // ------------------------------------------------------------------ mu
-// mu at (x, y, storage plane zs) from phi, op order of the oracle orc_mu:
 // mu = (A phi + B phi^3) - kappa lap, lap = (((((phi(x+1) + phi(x-1)) + phi(y+1))
-//      + phi(y-1)) + phi(z+1)) + phi(z-1)) - 6 phi.
-__device__ __forceinline__ double mu_at(const double *phi, const FluidArgs &a, int x, int y,
-                                        long long zs) {
-    const double *c = phi + zs * a.PL;
-    const long long r = (long long)y * a.nx;
-    const double ph = __ldg(c + r + x);
-    double s = __ldg(c + r + wrapi(x + 1, a.nx));
-    s = __dadd_rn(s, __ldg(c + r + wrapi(x - 1, a.nx)));
-    s = __dadd_rn(s, __ldg(c + (long long)wrapi(y + 1, a.ny) * a.nx + x));
-    s = __dadd_rn(s, __ldg(c + (long long)wrapi(y - 1, a.ny) * a.nx + x));
-    s = __dadd_rn(s, __ldg(c + a.PL + r + x));
-    s = __dadd_rn(s, __ldg(c - a.PL + r + x));
-    const double lap = __dsub_rn(s, __dmul_rn(6.0, ph));
-    const double p3 = __dmul_rn(__dmul_rn(ph, ph), ph);
-    return __dsub_rn(__dadd_rn(__dmul_rn(a.A, ph), __dmul_rn(a.B, p3)), __dmul_rn(a.kappa, lap));
-}
-
-// Observable mu on owned planes (needs phi halos of depth >= 1).
+//      + phi(y-1)) + phi(z+1)) + phi(z-1)) - 6 phi   (oracle orc_mu op order)
 template <int VVL>
 __global__ void __launch_bounds__(256) k_mu(const FluidArgs a) {
     Pos p;
     if (!thread_pos<VVL>(a, p)) return;
+    const double *c = a.phi_in + (long long)(p.z + 1) * a.PL;
+    const int yp = wrapi(p.y + 1, a.ny), ym = wrapi(p.y - 1, a.ny);
     double mu[VVL];
 #pragma unroll
-    for (int k = 0; k < VVL; ++k) mu[k] = mu_at(a.phi_in, a, p.x0 + k, p.y, p.z + kSOff);
-    store_vec<VVL>(a.mu_out + (long long)(p.z + kSOff) * a.PL + (long long)p.y * a.nx + p.x0, mu);
+    for (int k = 0; k < VVL; ++k) {
+        const int x = p.x0 + k;
+        const int xp = wrapi(x + 1, a.nx), xm = wrapi(x - 1, a.nx);
+        const double ph = __ldg(c + (long long)p.y * a.nx + x);
+        double s = __ldg(c + (long long)p.y * a.nx + xp);
+        s = __dadd_rn(s, __ldg(c + (long long)p.y * a.nx + xm));
+        s = __dadd_rn(s, __ldg(c + (long long)yp * a.nx + x));
+        s = __dadd_rn(s, __ldg(c + (long long)ym * a.nx + x));
+        s = __dadd_rn(s, __ldg(c + a.PL + (long long)p.y * a.nx + x));
+        s = __dadd_rn(s, __ldg(c - a.PL + (long long)p.y * a.nx + x));
+        const double lap = __dsub_rn(s, __dmul_rn(6.0, ph));
+        const double p3 = __dmul_rn(__dmul_rn(ph, ph), ph);
+        mu[k] = __dsub_rn(__dadd_rn(__dmul_rn(a.A, ph), __dmul_rn(a.B, p3)),
+                          __dmul_rn(a.kappa, lap));
+    }
+    const long long off = (long long)p.y * a.nx + p.x0;
+    store_vec<VVL>(a.mu_out + (long long)(p.z + 1) * a.PL + off, mu);
+    if (a.wrap) {
+        if (p.z == 0) store_vec<VVL>(a.mu_out + (long long)(a.nzl + 1) * a.PL + off, mu);
+        if (p.z == a.nzl - 1) store_vec<VVL>(a.mu_out + off, mu);
+    }
 }
 
 // ------------------------------------------------------------------ collide-stream
@@ -257,27 +247,6 @@ __global__ void __launch_bounds__(256) k_collide_stream(const FluidArgs a) {
     Pos p;
     if (!thread_pos<VVL>(a, p)) return;
 
-    // mu at the site and its 6 neighbours straight from phi (radius-2
-    // stencil, L1/L2 resident): no mu array round trip through HBM.  Done
-    // before the 38 pulls so the stencil's registers are free again.
-    const long long zs = p.z + kSOff;
-    double gm[VVL][4];  // mu, d/dx, d/dy, d/dz
-#pragma unroll
-    for (int k = 0; k < VVL; ++k) {
-        gm[k][0] = gm[k][1] = gm[k][2] = gm[k][3] = 0.0;
-        if constexpr (PHYS == 1) {
-            const int x = p.x0 + k, y = p.y;
-            const double *ph = a.phi_in;
-            gm[k][0] = mu_at(ph, a, x, y, zs);
-            gm[k][1] = Exact::mul(Exact::sub(mu_at(ph, a, wrapi(x + 1, a.nx), y, zs),
-                                             mu_at(ph, a, wrapi(x - 1, a.nx), y, zs)), 0.5);
-            gm[k][2] = Exact::mul(Exact::sub(mu_at(ph, a, x, wrapi(y + 1, a.ny), zs),
-                                             mu_at(ph, a, x, wrapi(y - 1, a.ny), zs)), 0.5);
-            gm[k][3] = Exact::mul(Exact::sub(mu_at(ph, a, x, y, zs + 1),
-                                             mu_at(ph, a, x, y, zs - 1)), 0.5);
-        }
-    }
-
     double F[Q][VVL], G[Q][VVL];
     static_for<0, Q>([&](auto I) { pull<I.value, VVL>(F[I.value], a.f_in, a, p); });
     static_for<0, Q>([&](auto I) { pull<I.value, VVL>(G[I.value], a.g_in, a, p); });
@@ -291,12 +260,23 @@ __global__ void __launch_bounds__(256) k_collide_stream(const FluidArgs a) {
         for (int k = 0; k < VVL; ++k) faccum<I.value, M>(st[k], F[I.value][k]);
     });
     bool ok[VVL];
+    const double *mc = a.mu + (long long)(p.z + 1) * a.PL;
+    const int yp = wrapi(p.y + 1, a.ny), ym = wrapi(p.y - 1, a.ny);
 #pragma unroll
     for (int k = 0; k < VVL; ++k) {
 #pragma unroll
         for (int i = 0; i < Q; ++i) st[k].phi = M::add(st[k].phi, G[i][k]);
-        st[k].mu = gm[k][0];
-        const double gmx = gm[k][1], gmy = gm[k][2], gmz = gm[k][3];
+        double gmx = 0.0, gmy = 0.0, gmz = 0.0;
+        if constexpr (PHYS == 1) {
+            const int x = p.x0 + k;
+            const long long r = (long long)p.y * a.nx;
+            st[k].mu = __ldg(mc + r + x);
+            gmx = Exact::mul(Exact::sub(__ldg(mc + r + wrapi(x + 1, a.nx)),
+                                        __ldg(mc + r + wrapi(x - 1, a.nx))), 0.5);
+            gmy = Exact::mul(Exact::sub(__ldg(mc + (long long)yp * a.nx + x),
+                                        __ldg(mc + (long long)ym * a.nx + x)), 0.5);
+            gmz = Exact::mul(Exact::sub(__ldg(mc + a.PL + r + x), __ldg(mc - a.PL + r + x)), 0.5);
+        }
         ok[k] = !(st[k].rho <= 0.0);
         if (ok[k]) {
             fsite_finish<MODE, PHYS>(st[k], gmx, gmy, gmz, a);

@@ -231,25 +231,18 @@ class BinaryFluid:
         return f, g
 
     def order_parameter(self) -> tuple[np.ndarray, np.ndarray]:
-        """(phi, mu) of the last step over the owned planes, shape (nzl, ny, nx).
-
-        phi is what the step used; mu is evaluated from it on demand by the
-        same device function the collision uses (ltk_fluid_mu), so it is
-        bitwise the chemical potential that drove the last collision."""
+        """(phi, mu) of the last step over the owned planes, shape (nzl, ny, nx)."""
         s = self.shape
         PL = s.nx * s.ny
         ptrs = [ctypes.c_void_p() for _ in range(4)]
         nat.lib.ltk_fluid_buffers(self._h, *[ctypes.byref(p) for p in ptrs])
-        nat.check(nat.lib.ltk_fluid_mu(ctypes.byref(self.slab), ptrs[2].value, ptrs[3].value,
-                                       ctypes.byref(self._params), 0, self.nzl, self.stream),
-                  "ltk_fluid_mu")
         out = []
         for p in (ptrs[2], ptrs[3]):
-            a = np.empty((self.nzl + 4) * PL)
+            a = np.empty((self.nzl + 2) * PL)
             nat.check(nat.lib.ltk_d2h(a.ctypes.data, p.value, a.nbytes, self.stream), "D2H")
             out.append(a)
         self.sync()
-        return tuple(a[2 * PL:(self.nzl + 2) * PL].reshape(self.nzl, s.ny, s.nx) for a in out)
+        return tuple(a[PL:(self.nzl + 1) * PL].reshape(self.nzl, s.ny, s.nx) for a in out)
 
     # -- stepping ------------------------------------------------------------
 

@@ -48,14 +48,13 @@ def neighbours(rank: int, nranks: int) -> tuple[int, int]:
 class HaloOp:
     """One point-to-point transfer of a halo plane.
 
-    kind: "f" / "g" (distribution component `comp`) or "phi".
-    plane: storage plane index zs (distributions: owned z = zs - 1;
-    phi: owned z = zs - 2).
+    kind: "fg" (distribution component `comp` of dist "f" or "g"), "phi", "mu".
+    plane: storage plane index zs (owned z = zs - 1; 0 and nzl + 1 are halos).
     """
 
     op: str        # "send" | "recv"
     peer: int
-    kind: str      # "f", "g", "phi"
+    kind: str      # "f", "g", "phi", "mu"
     comp: int      # distribution component (or 0 for phi/mu)
     plane: int
 
@@ -63,12 +62,9 @@ class HaloOp:
 def halo_schedule(kind: str, rank: int, nranks: int, nzl: int) -> list[HaloOp]:
     """Ordered ops of one exchange group, exactly as the engine issues them.
 
-    kind "fg" (distributions, halo depth 1, storage zs = z + 1): crossing
-    components of f then g; the top owned plane (zs = nzl) goes up, the bottom
-    one (zs = 1) down; receives land in zs = 0 (from down), zs = nzl+1 (from up).
-    kind "phi" (scalar, halo depth 2, storage zs = z + 2): owned planes
-    nzl-2, nzl-1 (zs = nzl, nzl+1) go up, owned 0, 1 (zs = 2, 3) go down;
-    receives land in zs = 0, 1 (from down) and zs = nzl+2, nzl+3 (from up).
+    kind "fg": crossing components of f then g; "phi" / "mu": one plane each way.
+    Sends: top owned plane (zs = nzl) up, bottom owned plane (zs = 1) down.
+    Receives: from down into zs = 0, from up into zs = nzl + 1.
     """
     up, down = neighbours(rank, nranks)
     ops: list[HaloOp] = []
@@ -81,15 +77,9 @@ def halo_schedule(kind: str, rank: int, nranks: int, nzl: int) -> list[HaloOp]:
             ops += [HaloOp("recv", down, d, c, 0) for c in CZ_UP]
         for d in ("f", "g"):
             ops += [HaloOp("recv", up, d, c, nzl + 1) for c in CZ_DOWN]
-    elif kind == "phi":
-        if nzl < 2:
-            raise ShapeError("phi halos of depth 2 need >= 2 planes per rank")
-        ops = ([HaloOp("send", up, kind, 0, nzl + k) for k in (0, 1)] +
-               [HaloOp("send", down, kind, 0, 2 + k) for k in (0, 1)] +
-               [HaloOp("recv", down, kind, 0, k) for k in (0, 1)] +
-               [HaloOp("recv", up, kind, 0, nzl + 2 + k) for k in (0, 1)])
     else:
-        raise ShapeError(f"unknown halo kind {kind!r}")
+        ops = [HaloOp("send", up, kind, 0, nzl), HaloOp("send", down, kind, 0, 1),
+               HaloOp("recv", down, kind, 0, 0), HaloOp("recv", up, kind, 0, nzl + 1)]
     return ops
 
 
@@ -126,8 +116,6 @@ class VirtualSlabs:
         nat.check(nat.lib.ltk_set_device(device))
         self.stream = nat.stream_create()
         z0, nzl = slab_bounds(shape.nz, 0, nslabs)
-        if nzl < 2:
-            raise ShapeError("phi halos of depth 2 need >= 2 planes per slab")
         PL = shape.nx * shape.ny
         self.nzl, self.PL = nzl, PL
         cstride = -(-((nzl + 2) * PL) // 64) * 64
@@ -136,7 +124,8 @@ class VirtualSlabs:
         self.bufs = []
         for _ in range(nslabs):
             b = {k: self._alloc(8 * Q * cstride) for k in ("fA", "gA", "fB", "gB")}
-            b["phi"] = self._alloc(8 * (nzl + 4) * PL)
+            b["phi"] = self._alloc(8 * (nzl + 2) * PL)
+            b["mu"] = self._alloc(8 * (nzl + 2) * PL)
             self.bufs.append(b)
         self.face = self._alloc(8 * 10 * PL)
         self.cur = "A"
@@ -202,16 +191,14 @@ class VirtualSlabs:
                 nat.check(nat.lib.ltk_fluid_unpack_face(sl, pb["f" + s], pb["g" + s], self.face,
                                                         direction, self.stream))
 
-    def _exchange_phi(self) -> None:
-        """Depth-2 phi halos: owned planes nzl-2, nzl-1 -> up's zs 0, 1;
-        owned 0, 1 -> down's zs nzl+2, nzl+3 (storage zs = z + 2)."""
+    def _exchange_plane(self, key: str) -> None:
         nb = 8 * self.PL
         for r, b in enumerate(self.bufs):
             up, down = neighbours(r, self.P)
-            nat.check(nat.lib.ltk_d2d(self.bufs[up]["phi"], b["phi"] + self.nzl * nb, 2 * nb,
+            top, bot = b[key] + self.nzl * nb, b[key] + nb
+            nat.check(nat.lib.ltk_d2d(self.bufs[up][key], top, nb, self.stream))
+            nat.check(nat.lib.ltk_d2d(self.bufs[down][key] + (self.nzl + 1) * nb, bot, nb,
                                       self.stream))
-            nat.check(nat.lib.ltk_d2d(self.bufs[down]["phi"] + (self.nzl + 2) * nb,
-                                      b["phi"] + 2 * nb, 2 * nb, self.stream))
 
     def run(self, nsteps: int) -> None:
         sl = ctypes.byref(self.slab)
@@ -222,10 +209,15 @@ class VirtualSlabs:
             for b in self.bufs:
                 nat.check(nat.lib.ltk_fluid_phi(sl, b["g" + s], b["phi"], 0, self.nzl,
                                                 self.stream), "phi")
-            self._exchange_phi()
+            self._exchange_plane("phi")
+            if self.params.physics == 1:
+                for b in self.bufs:
+                    nat.check(nat.lib.ltk_fluid_mu(sl, b["phi"], b["mu"], prm, 0, self.nzl,
+                                                   self.stream), "mu")
+                self._exchange_plane("mu")
             for b in self.bufs:
                 nat.check(nat.lib.ltk_fluid_collide_stream(
-                    sl, b["f" + s], b["g" + s], b["phi"], b["f" + o], b["g" + o], prm, 0,
+                    sl, b["f" + s], b["g" + s], b["mu"], b["f" + o], b["g" + o], prm, 0,
                     self.nzl, self.vvl, self.stream), "collide_stream")
             self.cur = o
         site = ctypes.c_int64(-1)

@@ -16,7 +16,7 @@ import pytest
 
 from conftest import ROOT
 
-SHAPE = (6, 5, 12)  # nz 12: 6 planes per rank at P=2, 4 at P=3
+SHAPE = (6, 5, 12)
 STEPS = 3
 
 
@@ -76,7 +76,8 @@ def _worker(rank, world, port, out_q):
         return s
 
     f, g = to_slab(f0), to_slab(g0)
-    phi = np.zeros((nzl + 4, ny, nx))  # scalar storage zs = z + 2, halo depth 2
+    phi = np.zeros((nzl + 2, ny, nx))
+    mu = np.zeros((nzl + 2, ny, nx))
     cv = orc.CV
     for _ in range(STEPS):
         _exchange(dist, torch, {"f": f, "g": g}, halo_schedule("fg", rank, world, nzl), rank)
@@ -87,13 +88,12 @@ def _worker(rank, world, port, out_q):
         ph = np.zeros((nzl, ny, nx))
         for i in range(19):
             ph = ph + gs[i]
-        phi[2:nzl + 2] = ph
+        phi[1:nzl + 1] = ph
         _exchange(dist, torch, {"phi": phi}, halo_schedule("phi", rank, world, nzl), rank)
-        # mu on owned planes +- 1 from the depth-2 phi halos (as the kernel does)
-        pz = phi[1:nzl + 3]
-        nb = [np.roll(pz, -1, 2), np.roll(pz, 1, 2), np.roll(pz, -1, 1), np.roll(pz, 1, 1)]
-        mu = np.zeros((nzl + 2, ny, nx))
-        mu[:] = orc.mu_numpy(pz, nb + [phi[2:nzl + 4], phi[0:nzl + 2]], prm)
+        nb = [np.roll(ph, -1, 2), np.roll(ph, 1, 2), np.roll(ph, -1, 1), np.roll(ph, 1, 1),
+              phi[2:nzl + 2], phi[0:nzl]]
+        mu[1:nzl + 1] = orc.mu_numpy(ph, nb, prm)
+        _exchange(dist, torch, {"mu": mu}, halo_schedule("mu", rank, world, nzl), rank)
         m = mu[1:nzl + 1]
         grad = [(np.roll(m, -1, 2) - np.roll(m, 1, 2)) * 0.5,
                 (np.roll(m, -1, 1) - np.roll(m, 1, 1)) * 0.5,
