@@ -64,29 +64,52 @@ __device__ __forceinline__ void finish_site(Site &s, const CollideArgs &a) {
     }
 }
 
-// Relax component I of both distributions at one site.
-// T1: bit 0 = tau_f == 1.0, bit 1 = tau_g == 1.0 (EXACT only)
-template <int I, int MODE, int T1>
-__device__ __forceinline__ void relax(double &f, double &g, const Site &s, const CollideArgs &a) {
+// Relax component I of both distributions at one site.  EXACT: q = (u.c)/cs2
+// and sq = ((u.c)(u.c))/((2 cs2) cs2) are passed in, because the opposite
+// velocity reuses them: dot_c gives u.c_opp == -(u.c) exactly (RN is symmetric
+// under negation), so (u.c_opp)/cs2 == -q and its square term == sq, and the
+// bracket ((1 + q) + sq) - t is then bit-identical to the reference's.
+// T1: bit 0 = tau_f == 1.0, bit 1 = tau_g == 1.0 (EXACT only).
+template <int I, int T1>
+__device__ __forceinline__ void relax_exact(double &f, double &g, double q, double sq,
+                                            const Site &s, const CollideArgs &a) {
+    using M = Exact;
+    const double br = M::sub(M::add(M::add(1.0, q), sq), s.t);
+    const double feq = M::mul(M::mul(a.wv[I], s.rho), br);
+    const double geq = M::mul(M::mul(a.wv[I], s.phi), br);
+    const double df = M::sub(f, feq), dg = M::sub(g, geq);
+    if constexpr (T1 & 1) f = M::sub(f, df);  // x / 1.0 == x
+    else f = M::sub(f, M::div(df, a.tau_f));
+    if constexpr (T1 & 2) g = M::sub(g, dg);
+    else g = M::sub(g, M::div(dg, a.tau_g));
+}
+
+template <int I>
+__device__ __forceinline__ void relax_fast(double &f, double &g, const Site &s,
+                                           const CollideArgs &a) {
+    const double ud = dot_c<cx(I), cy(I), cz(I), Fast>(s.ux, s.uy, s.uz);
+    const double br = fma(ud, fma(ud, a.a2, a.a1), s.t);
+    const double feq = (a.wv[I] * s.rho) * br;
+    const double geq = (a.wv[I] * s.phi) * br;
+    f = fma(feq - f, a.inv_tau_f, f);
+    g = fma(geq - g, a.inv_tau_g, g);
+}
+
+// Relax the pair {C, opp(C)} (C canonical) of site v.
+template <int C, int MODE, int T1, int W>
+__device__ __forceinline__ void relax_pair(double (&F)[Q][W], double (&G)[Q][W], int v,
+                                           const Site &s, const CollideArgs &a) {
+    constexpr int O = opp(C);
     if constexpr (MODE == LTK_MODE_EXACT) {
         using M = Exact;
-        double ud = dot_c<cx(I), cy(I), cz(I), M>(s.ux, s.uy, s.uz);
-        double br = M::sub(M::add(M::add(1.0, M::div(ud, a.cs2)), M::div(M::mul(ud, ud), a.c2)),
-                           s.t);
-        double feq = M::mul(M::mul(a.wv[I], s.rho), br);
-        double geq = M::mul(M::mul(a.wv[I], s.phi), br);
-        const double df = M::sub(f, feq), dg = M::sub(g, geq);
-        if constexpr (T1 & 1) f = M::sub(f, df);
-        else f = M::sub(f, M::div(df, a.tau_f));
-        if constexpr (T1 & 2) g = M::sub(g, dg);
-        else g = M::sub(g, M::div(dg, a.tau_g));
+        const double ud = dot_c<cx(C), cy(C), cz(C), M>(s.ux, s.uy, s.uz);
+        const double q = M::div(ud, a.cs2);
+        const double sq = M::div(M::mul(ud, ud), a.c2);
+        relax_exact<C, T1>(F[C][v], G[C][v], q, sq, s, a);
+        if constexpr (O != C) relax_exact<O, T1>(F[O][v], G[O][v], -q, sq, s, a);
     } else {
-        double ud = dot_c<cx(I), cy(I), cz(I), Fast>(s.ux, s.uy, s.uz);
-        double br = fma(ud, fma(ud, a.a2, a.a1), s.t);
-        double feq = (a.wv[I] * s.rho) * br;
-        double geq = (a.wv[I] * s.phi) * br;
-        f = fma(feq - f, a.inv_tau_f, f);
-        g = fma(geq - g, a.inv_tau_g, g);
+        relax_fast<C>(F[C][v], G[C][v], s, a);
+        if constexpr (O != C) relax_fast<O>(F[O][v], G[O][v], s, a);
     }
 }
 
@@ -124,10 +147,11 @@ __device__ __forceinline__ void collide_sites(double *__restrict__ f, double *__
             finish_site<MODE>(st[v], a);
         }
     }
-    static_for<0, Q>([&](auto I) {
+    static_for<0, 10>([&](auto K) {
+        constexpr int C = kCanon[K.value];
 #pragma unroll
         for (int v = 0; v < W; ++v)
-            if (st[v].ok) relax<I.value, MODE, T1>(F[I.value][v], G[I.value][v], st[v], a);
+            if (st[v].ok) relax_pair<C, MODE, T1, W>(F, G, v, st[v], a);
     });
     // padding lanes (rho <= 0) are written back unchanged: bitwise untouched
 #pragma unroll

@@ -197,14 +197,16 @@ __device__ __forceinline__ void fsite_finish(FSite &s, double gmx, double gmy, d
     }
 }
 
-// T1 (EXACT): bit 0 = tau_f == 1.0, bit 1 = tau_g == 1.0 -> x / 1.0 == x, skip it
+// T1 (EXACT): bit 0 = tau_f == 1.0, bit 1 = tau_g == 1.0 -> x / 1.0 == x, skip it.
+// EXACT: q = (u.c)/cs2 and sq = ((u.c)(u.c))/((2cs2)cs2) come from the pair's
+// canonical velocity; the opposite velocity gets -q and sq, which leaves the
+// bracket ((1 + q) + sq) - t bit-identical (see collide.cu relax_exact).
 template <int I, int MODE, int PHYS, int T1>
-__device__ __forceinline__ void frelax(double &f, double &g, const FSite &s, const FluidArgs &a) {
+__device__ __forceinline__ void frelax(double &f, double &g, double q, double sq, const FSite &s,
+                                       const FluidArgs &a) {
     if constexpr (MODE == LTK_MODE_EXACT) {
         using M = Exact;
-        const double ud = dot_c<cx(I), cy(I), cz(I), M>(s.ux, s.uy, s.uz);
-        const double br = M::sub(
-            M::add(M::add(1.0, M::div(ud, a.cs2)), M::div(M::mul(ud, ud), a.c2)), s.t);
+        const double br = M::sub(M::add(M::add(1.0, q), sq), s.t);
         const double feq = M::mul(M::mul(a.wv[I], s.rho), br);
         double geq = M::mul(M::mul(a.wv[I], s.phi), br);
         const double df = M::sub(f, feq);
@@ -212,6 +214,7 @@ __device__ __forceinline__ void frelax(double &f, double &g, const FSite &s, con
         if constexpr (T1 & 1) fn = M::sub(f, df);
         else fn = M::sub(f, M::div(df, a.tau_f));
         if constexpr (PHYS == 1) {
+            const double ud = dot_c<cx(I), cy(I), cz(I), M>(s.ux, s.uy, s.uz);
             const double cF = dot_c<cx(I), cy(I), cz(I), M>(s.Fx, s.Fy, s.Fz);
             const double src =
                 M::mul(M::mul(a.srcpre, a.wv[I]),
@@ -241,8 +244,24 @@ __device__ __forceinline__ void frelax(double &f, double &g, const FSite &s, con
     }
 }
 
+// Relax the pair {C, opp(C)} (C canonical) of lane k.
+template <int C, int MODE, int PHYS, int T1, int VVL>
+__device__ __forceinline__ void frelax_pair(double (&F)[Q][VVL], double (&G)[Q][VVL], int k,
+                                            const FSite &s, const FluidArgs &a) {
+    constexpr int O = opp(C);
+    double q = 0.0, sq = 0.0;
+    if constexpr (MODE == LTK_MODE_EXACT) {
+        using M = Exact;
+        const double ud = dot_c<cx(C), cy(C), cz(C), M>(s.ux, s.uy, s.uz);
+        q = M::div(ud, a.cs2);
+        sq = M::div(M::mul(ud, ud), a.c2);
+    }
+    frelax<C, MODE, PHYS, T1>(F[C][k], G[C][k], q, sq, s, a);
+    if constexpr (O != C) frelax<O, MODE, PHYS, T1>(F[O][k], G[O][k], -q, sq, s, a);
+}
+
 template <int VVL, int MODE, int PHYS, int T1>
-__global__ void __launch_bounds__(256) k_collide_stream(const FluidArgs a) {
+__global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_collide_stream(const FluidArgs a) {
     using M = typename std::conditional<MODE == LTK_MODE_EXACT, Exact, Fast>::type;
     Pos p;
     if (!thread_pos<VVL>(a, p)) return;
@@ -286,10 +305,11 @@ __global__ void __launch_bounds__(256) k_collide_stream(const FluidArgs a) {
             flag_singular(a.err, site);
         }
     }
-    static_for<0, Q>([&](auto I) {
+    static_for<0, 10>([&](auto K) {
+        constexpr int C = kCanon[K.value];
 #pragma unroll
         for (int k = 0; k < VVL; ++k)
-            if (ok[k]) frelax<I.value, MODE, PHYS, T1>(F[I.value][k], G[I.value][k], st[k], a);
+            if (ok[k]) frelax_pair<C, MODE, PHYS, T1, VVL>(F, G, k, st[k], a);
     });
 
     const long long off = (long long)p.y * a.nx + p.x0;

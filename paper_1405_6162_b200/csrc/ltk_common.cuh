@@ -60,6 +60,15 @@ __host__ __device__ constexpr int cz(int i) {
     return t[i];
 }
 
+// Opposite velocity, c_opp(i) = -c_i (reference model.py:62-68 negation_index).
+__host__ __device__ constexpr int opp(int i) {
+    constexpr int t[Q] = {0, 2, 1, 4, 3, 6, 5, 10, 9, 8, 7, 14, 13, 12, 11, 18, 17, 16, 15};
+    return t[i];
+}
+
+// The 10 canonical members of {i, opp(i)} (the smaller index; 0 is its own).
+constexpr int kCanon[10] = {0, 1, 3, 5, 7, 8, 11, 12, 15, 16};
+
 // Sum of ci*u over the nonzero velocity components, in x, y, z order.  The
 // reference evaluates ((ux*cx + uy*cy) + uz*cz) with cx..cz in {0, +-1}:
 // products by +-1 are exact and adding a +-0 product never changes a value
