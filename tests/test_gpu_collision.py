@@ -275,3 +275,89 @@ class TestBenchApi:
         lines = lk.report_best(rows)
         assert lines[0].startswith("binary-collision/cuda: best VVL=")
         assert lk.emit_csv(rows).startswith("kernel,backend,nx,ny,nz,vvl,workers,tpb,iters")
+
+
+class TestEdgeCases:
+    def test_ragged_and_tiny_lattices_bitwise(self, lk):
+        from oracle import oracle as orc
+        from paper_1405_6162_b200.verify import run_framework_collision
+
+        for shape in ((1, 1, 1), (5, 7, 3), (1, 1, 17), (9, 1, 1)):
+            f0, g0 = _state(lk, shape, 8)
+            n, P = f0.descriptor.nsites, f0.descriptor.padded_sites
+            for vvl in (1, 2, 4, 8, 16):
+                f1, g1 = run_framework_collision(f0, g0, "cuda", vvl, 1, steps=2)
+                rf, rg = f0.data.copy(), g0.data.copy()
+                orc.collide(rf, rg, P, n, steps=2)
+                assert np.array_equal(f1.data, rf) and np.array_equal(g1.data, rg), (shape, vvl)
+
+    def test_partial_chunk_range(self, lk):
+        # a launch over a sub-range of chunks touches exactly those sites
+        from paper_1405_6162_b200 import _native as nat
+        import ctypes
+
+        f0, g0 = _state(lk, (8, 8, 8), 3)
+        P = f0.descriptor.padded_sites
+        dev = lk.TargetDevice()
+        bf, bg = lk.target_malloc(dev, f0.descriptor), lk.target_malloc(dev, g0.descriptor)
+        lk.copy_to_target(bf, f0)
+        lk.copy_to_target(bg, g0)
+        m = lk.D3Q19Model()
+        prm = lk.kernels.collision_params(m.wv, m.cs2, 1.0, 1.0)
+        nat.check(nat.lib.ltk_collide(10, 20, 4, 128, bf.ptr, bg.ptr, P, 512, ctypes.byref(prm),
+                                      dev.stream))
+        lk.sync_target(dev)
+        out = lk.field_create(f0.descriptor)
+        lk.copy_from_target(out, bf)
+        from oracle import oracle as orc
+        rf, rg = f0.data.copy(), g0.data.copy()
+        orc.lib().orc_collide(orc._p(rf), orc._p(rg), P, 512, orc._p(orc.WV),
+                              orc._p(orc.CV.astype(float)), orc.CS2, 1.0, 1.0, 40, 80)
+        assert np.array_equal(out.data, rf)
+
+    def test_nan_input_propagates_like_reference(self, lk):
+        from oracle import oracle as orc
+        from paper_1405_6162_b200.verify import run_framework_collision
+
+        f0, g0 = _state(lk, (4, 4, 4), 1)
+        f0.data[5] = np.nan      # comp 0 of site 5
+        g0.data[64 * 3 + 9] = np.inf
+        f1, g1 = run_framework_collision(f0, g0, "cuda", 1, 1)
+        rf, rg = f0.data.copy(), g0.data.copy()
+        orc.collide(rf, rg, 64, 64)
+        assert np.array_equal(np.isnan(f1.data), np.isnan(rf))
+        fin = np.isfinite(rf)
+        assert np.array_equal(f1.data[fin], rf[fin])
+
+    def test_invalid_plans_rejected(self, lk):
+        f0, g0 = _state(lk, (4, 4, 4), 1)
+        dev = lk.TargetDevice()
+        lk.set_model_constants(dev, lk.D3Q19Model())
+        bf, bg = lk.target_malloc(dev, f0.descriptor), lk.target_malloc(dev, g0.descriptor)
+        with pytest.raises(lk.PlanError):
+            lk.launch(dev, lk.binary_collision_kernel, lk.LaunchPlan(extent=128, vvl=2), [bf, bg])
+        with pytest.raises(lk.PlanError):  # VVL 32 not compiled
+            lk.launch(dev, lk.binary_collision_kernel, lk.LaunchPlan(extent=64, vvl=32), [bf, bg])
+        other = lk.TargetDevice()
+        with pytest.raises(lk.DeviceError):
+            lk.launch(other, lk.binary_collision_kernel, lk.LaunchPlan(extent=64, vvl=2), [bf, bg])
+
+
+class TestStress:
+    def test_repeated_golden_runs_are_stable(self, lk, golden):
+        # guards against order-dependent nondeterminism: the 8^3 golden case,
+        # 40 times over VVL 1/2 and two TPBs, interleaved with a large launch
+        from paper_1405_6162_b200.verify import run_framework_collision
+
+        meta, _ = golden
+        case = meta["collision"][0]
+        model = lk.D3Q19Model()
+        f0, g0 = _state(lk, case["shape"], case["seed"], model)
+        big_f, big_g = _state(lk, (128, 128, 64), 2, model)
+        for k in range(40):
+            vvl, tpb = (1, 2)[k % 2], (128, 256)[(k // 2) % 2]
+            f1, g1 = run_framework_collision(f0, g0, "cuda", vvl, 1, steps=case["steps"],
+                                             model=model, tpb=tpb)
+            assert sha(f1.data) == case["out_f"] and sha(g1.data) == case["out_g"], (k, vvl, tpb)
+            if k % 10 == 0:
+                run_framework_collision(big_f, big_g, "cuda", 2, 1, steps=1, model=model)

@@ -154,3 +154,56 @@ class TestSlabDecomposition:
         vs.close()
         of, og, _, _ = _oracle(f0, g0, shape, 3, 1)
         assert np.array_equal(f1.data, of) and np.array_equal(g1.data, og)
+
+
+class TestFullSizeProperties:
+    """BASELINE sizes through size-independent properties (north-star tolerance)."""
+
+    def test_256cube_exact_vs_oracle_and_fast(self, lk):
+        # configs[2]: one EXACT step bitwise vs the oracle, FAST within 1e-12
+        shape = (256, 256, 256)
+        f0, g0 = _state(lk, shape, 1234)
+        ex = {}
+        for mode in (lk.MODE_EXACT, lk.MODE_FAST):
+            with lk.BinaryFluid(lk.LatticeShape(*shape), mode=mode) as sim:
+                sim.load(f0, g0)
+                sim.run(2)
+                ex[mode] = sim.fields()
+        of, og, _, _ = _oracle(f0, g0, shape, 2, 1)
+        assert np.array_equal(ex[lk.MODE_EXACT][0].data, of)
+        assert np.array_equal(ex[lk.MODE_EXACT][1].data, og)
+        for got, ref in ((ex[lk.MODE_FAST][0].data, of), (ex[lk.MODE_FAST][1].data, og)):
+            rel = np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300))
+            assert rel <= 1e-12, rel
+
+    def test_256cube_long_run_conservation(self, lk):
+        # 200 FAST steps: total mass and total phi conserved to rounding
+        shape = lk.LatticeShape(256, 256, 256)
+        f0, g0 = _state(lk, (256, 256, 256), 99)
+        n, P = shape.nsites, f0.descriptor.padded_sites
+        m0 = f0.data.reshape(19, P)[:, :n].sum(dtype=np.float64)
+        p0 = g0.data.reshape(19, P)[:, :n].sum(dtype=np.float64)
+        with lk.BinaryFluid(shape, mode=lk.MODE_FAST) as sim:
+            sim.load(f0, g0)
+            sim.run(200)
+            f1, g1 = sim.fields()
+        m1 = f1.data.reshape(19, P)[:, :n].sum(dtype=np.float64)
+        p1 = g1.data.reshape(19, P)[:, :n].sum(dtype=np.float64)
+        assert abs(m1 - m0) <= 1e-10 * abs(m0)
+        assert abs(p1 - p0) <= 1e-10 * abs(p0)
+        assert np.all(np.isfinite(f1.data)) and np.all(np.isfinite(g1.data))
+
+    def test_ragged_shapes(self, lk):
+        # odd extents, nx not a multiple of the warp, planes of odd size
+        for shape in ((7, 6, 5), (33, 10, 3), (2, 2, 2), (64, 3, 9)):
+            f0, g0 = _state(lk, shape, 5)
+            with lk.BinaryFluid(lk.LatticeShape(*shape)) as sim:
+                sim.load(f0, g0)
+                sim.run(3)
+                f1, g1 = sim.fields()
+            of, og, _, _ = _oracle(f0, g0, shape, 3, 1)
+            assert np.array_equal(f1.data, of) and np.array_equal(g1.data, og), shape
+
+    def test_odd_plane_rejected(self, lk):
+        with pytest.raises(lk.ShapeError):
+            lk.BinaryFluid(lk.LatticeShape(3, 5, 4))
