@@ -15,7 +15,7 @@
 #include <new>
 #include <vector>
 
-#include "fluid_kernels.cuh"
+#include "stencil_tma.cuh"
 
 namespace ltk {
 
@@ -96,6 +96,21 @@ static int launch_phi(const FluidArgs &a, int vvl, cudaStream_t st) {
 
 static int launch_mu(const FluidArgs &a, int vvl, cudaStream_t st) {
     if (a.nthreads <= 0) return LTK_OK;
+    if (mu_tma_ok(a)) {
+        // shared-memory staged stencil, rows loaded by TMA bulk copies
+        static bool attr_set = false;
+        const size_t smem = mu_tma_smem(a);
+        if (!attr_set || smem > 48 * 1024) {
+            LTK_CUDA(cudaFuncSetAttribute(k_mu_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(200 * 1024)));
+            attr_set = true;
+        }
+        dim3 grid((unsigned)(a.ny / kMuTY), (unsigned)((a.nplanes + kMuZ - 1) / kMuZ));
+        const int threads = std::min(256, (a.nx + 31) / 32 * 32);
+        k_mu_tma<<<grid, threads, smem, st>>>(a);
+        LTK_CHECK_LAUNCH("k_mu_tma");
+        return LTK_OK;
+    }
     const unsigned g = grid_for(a.nthreads, kTPB);
     switch (vvl) {
         case 1: k_mu<1><<<g, kTPB, 0, st>>>(a); break;

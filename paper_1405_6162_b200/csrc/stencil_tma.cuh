@@ -1,0 +1,144 @@
+// stencil_tma.cuh -- chemical potential from a shared-memory staged phi tile,
+// rows brought in by the Tensor Memory Accelerator (cp.async.bulk, 1-D bulk
+// copies completing on an mbarrier).
+//
+// A CTA owns TY full x-rows and marches Z planes in z.  Its shared memory
+// holds a ring of plane slots, each (TY + 2) rows x nx doubles (the rows
+// y0-1 .. y0+TY, periodic in y): planes z-1, z, z+1 are read while the next
+// planes are in flight.  Every phi value therefore crosses HBM/L2 about
+// (TY+2)/TY * (Z+2)/Z times instead of once per stencil use, and the 7-point
+// reads hit shared memory.  x is periodic inside a row (index wrap in smem).
+// The arithmetic is mu_at's (fluid_kernels.cuh, oracle orc_mu op order), so
+// the result is bitwise identical to k_mu.
+#pragma once
+
+#include "fluid_kernels.cuh"
+
+namespace ltk {
+
+// Measured on the B200 at 256^3 (k_mu time per step): TY 8 / 4 slots 0.096 ms,
+// TY 4 / 6 slots 0.071 ms, TY 4 / 8 slots 0.084 ms, TY 2 / 8 slots 0.080 ms;
+// the unstaged k_mu took 0.107 ms.
+constexpr int kMuTY = 4;     // rows per CTA
+constexpr int kMuZ = 16;     // planes per CTA
+constexpr int kMuSlots = 6;  // plane ring: planes z-1..z+1 in use, 3 in flight
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on `bar`
+__device__ __forceinline__ void tma_row(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Issue the TY+2 row copies of storage plane zs into ring slot `slot`.
+__device__ __forceinline__ void load_plane(double *ring, uint64_t *bars, int slot, const FluidArgs &a,
+                                           int y0, int zs) {
+    const int nx = a.nx;
+    double *dst = ring + (size_t)slot * (kMuTY + 2) * nx;
+    const uint32_t row_bytes = (uint32_t)nx * 8u;
+    mbar_expect_tx(&bars[slot], row_bytes * (kMuTY + 2));
+    const double *plane = a.phi_in + (long long)zs * a.PL;
+    for (int r = 0; r < kMuTY + 2; ++r) {
+        const int y = wrapi(y0 - 1 + r, a.ny);
+        tma_row(dst + (size_t)r * nx, plane + (long long)y * nx, row_bytes, &bars[slot]);
+    }
+}
+
+// grid: (ny / kMuTY, ceil(nplanes / kMuZ)); block: up to 256 threads over x.
+__global__ void __launch_bounds__(256) k_mu_tma(const FluidArgs a) {
+    extern __shared__ __align__(128) double ring[];
+    __shared__ __align__(8) uint64_t bars[kMuSlots];
+    const int nx = a.nx;
+    const int y0 = blockIdx.x * kMuTY;
+    const int zb = a.z_lo + blockIdx.y * kMuZ;
+    const int ze = min(zb + kMuZ, a.z_lo + a.nplanes);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMuSlots; ++s) mbar_init(&bars[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // planes zb-1 .. ze (storage zs = z + 1) live in slot (z - zb + 1) % kMuSlots
+    const int first = zb - 1, last = ze;
+    if (threadIdx.x == 0)
+        for (int z = first; z <= min(last, first + kMuSlots - 1); ++z)
+            load_plane(ring, bars, (z - first) % kMuSlots, a, y0, z + 1);
+    const size_t slot_elems = (size_t)(kMuTY + 2) * nx;
+    for (int z = zb; z < ze; ++z) {
+        const int sm = (z - 1 - first) % kMuSlots, s0 = (z - first) % kMuSlots,
+                  sp = (z + 1 - first) % kMuSlots;
+        // k-th load of a slot completes phase k & 1
+        mbar_wait(&bars[sm], ((z - 1 - first) / kMuSlots) & 1);
+        mbar_wait(&bars[s0], ((z - first) / kMuSlots) & 1);
+        mbar_wait(&bars[sp], ((z + 1 - first) / kMuSlots) & 1);
+        const double *Pm = ring + sm * slot_elems, *P0 = ring + s0 * slot_elems,
+                     *Pp = ring + sp * slot_elems;
+        for (int r = 0; r < kMuTY; ++r) {
+            const int y = y0 + r;
+            const double *row = P0 + (size_t)(r + 1) * nx;
+            for (int x = threadIdx.x; x < nx; x += blockDim.x) {
+                const double ph = row[x];
+                double s = row[x + 1 < nx ? x + 1 : 0];
+                s = __dadd_rn(s, row[x > 0 ? x - 1 : nx - 1]);
+                s = __dadd_rn(s, row[x + nx]);       // y + 1
+                s = __dadd_rn(s, row[x - nx]);       // y - 1
+                s = __dadd_rn(s, Pp[(size_t)(r + 1) * nx + x]);  // z + 1
+                s = __dadd_rn(s, Pm[(size_t)(r + 1) * nx + x]);  // z - 1
+                const double lap = __dsub_rn(s, __dmul_rn(6.0, ph));
+                const double p3 = __dmul_rn(__dmul_rn(ph, ph), ph);
+                const double mu = __dsub_rn(__dadd_rn(__dmul_rn(a.A, ph), __dmul_rn(a.B, p3)),
+                                            __dmul_rn(a.kappa, lap));
+                const long long off = (long long)y * nx + x;
+                a.mu_out[(long long)(z + 1) * a.PL + off] = mu;
+                if (a.wrap) {
+                    if (z == 0) a.mu_out[(long long)(a.nzl + 1) * a.PL + off] = mu;
+                    if (z == a.nzl - 1) a.mu_out[off] = mu;
+                }
+            }
+        }
+        __syncthreads();  // every thread is done with plane z-1's slot
+        const int nz_next = z - 1 + kMuSlots;  // plane that reuses slot sm
+        if (threadIdx.x == 0 && nz_next <= last) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            load_plane(ring, bars, sm, a, y0, nz_next + 1);
+        }
+    }
+}
+
+inline bool mu_tma_ok(const FluidArgs &a) {
+    return a.ny % kMuTY == 0 && a.nx % 2 == 0 && (size_t)kMuSlots * (kMuTY + 2) * a.nx * 8 <=
+                                                       200 * 1024;
+}
+
+inline size_t mu_tma_smem(const FluidArgs &a) {
+    return (size_t)kMuSlots * (kMuTY + 2) * a.nx * 8;
+}
+
+}  // namespace ltk

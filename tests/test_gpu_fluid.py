@@ -207,3 +207,45 @@ class TestFullSizeProperties:
     def test_odd_plane_rejected(self, lk):
         with pytest.raises(lk.ShapeError):
             lk.BinaryFluid(lk.LatticeShape(3, 5, 4))
+
+
+class TestStencilKernels:
+    """The C-ABI stencil launchers against the oracle on random phi slabs
+    (k_mu_tma, the TMA/shared-memory staged stencil, when ny % 8 == 0 and nx
+    is even; the plain kernel otherwise)."""
+
+    @pytest.mark.parametrize("shape", [(256, 16, 37), (32, 8, 16), (2, 8, 5), (512, 24, 3),
+                                       (30, 16, 18), (12, 12, 7)])
+    def test_mu_matches_oracle(self, lk, shape):
+        import ctypes
+
+        from oracle import oracle as orc
+        from paper_1405_6162_b200 import _native as nat
+        from paper_1405_6162_b200.fluid import fluid_params
+
+        nx, ny, nz = shape
+        PL = nx * ny
+        rng = np.random.default_rng(nz)
+        phi_host = rng.random((nz, ny, nx)) * 2 - 1            # device order (z, y, x)
+        buf = np.zeros((nz + 2, ny, nx))
+        buf[1:nz + 1] = phi_host
+        buf[0], buf[nz + 1] = phi_host[nz - 1], phi_host[0]   # periodic halos
+        slab = nat.Slab(nx, ny, nz, -(-((nz + 2) * PL) // 64) * 64)
+        d_phi, d_mu = nat.malloc(buf.nbytes), nat.malloc(buf.nbytes)
+        try:
+            nat.check(nat.lib.ltk_h2d(d_phi, buf.ctypes.data, buf.nbytes, None))
+            prm = fluid_params()
+            for lo, hi in ((0, nz), (1, max(1, nz - 1))):
+                nat.check(nat.lib.ltk_fluid_mu(ctypes.byref(slab), d_phi, d_mu, ctypes.byref(prm),
+                                               lo, hi, None))
+                out = np.zeros_like(buf)
+                nat.check(nat.lib.ltk_d2h(out.ctypes.data, d_mu, out.nbytes, None))
+                nat.check(nat.lib.ltk_stream_sync(None))
+                ref = np.zeros(nx * ny * nz)
+                ph = np.ascontiguousarray(phi_host.transpose(2, 1, 0)).ravel()   # host (x, y, z)
+                orc.lib().orc_mu(orc._p(ph), orc._p(ref), nx, ny, nz, prm.A, prm.B, prm.kappa)
+                ref_dev = ref.reshape(nx, ny, nz).transpose(2, 1, 0)
+                assert np.array_equal(out[1 + lo:1 + hi], ref_dev[lo:hi]), (shape, lo, hi)
+        finally:
+            nat.free(d_phi)
+            nat.free(d_mu)
