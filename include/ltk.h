@@ -204,8 +204,9 @@ int ltk_fluid_gather(const ltk_slab *s, const double *slab, int64_t padded,
 typedef struct ltk_fluid ltk_fluid;
 
 /* Create a slab engine on the current device.  nranks == 1 -> periodic wrap
- * on one device; nranks > 1 -> NCCL halo exchange with ranks (rank+-1) mod
- * nranks (ltk_fluid_attach_nccl).  vvl: sites per thread of the fused
+ * on one device; nranks > 1 -> halo exchange with ranks (rank+-1) mod
+ * nranks, by peer stores from the kernels (ltk_fluid_attach_peers) or by
+ * NCCL (ltk_fluid_attach_nccl).  vvl: sites per thread of the fused
  * collide-stream kernel. */
 int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank,
                      int32_t nranks, const ltk_fluid_params *p, int32_t vvl,
@@ -232,6 +233,22 @@ int ltk_fluid_run(ltk_fluid *e, int64_t nsteps, void *stream);
 int ltk_fluid_use_graph(ltk_fluid *e, int32_t enable);
 /* Last step's per-kernel device times in ms (phi, mu, collide_stream, halo). */
 int ltk_fluid_profile(ltk_fluid *e, int32_t enable, float *ms4);
+
+/* Peer transport (one node, NVLink/NVSwitch): every slab exports its buffers
+ * with CUDA IPC (ltk_fluid_ipc_blob), the caller exchanges the blobs
+ * (torch.distributed) and attaches the slabs above and below.  The boundary
+ * planes' kernels then store their halo images directly into the neighbours'
+ * buffers (peer stores over NVLink) and progress counters pushed into the
+ * neighbours' inboxes order the phases -- the halo exchange is fused into the
+ * producing kernels.  Call before ltk_fluid_load. */
+#define LTK_IPC_BLOB_BYTES 512
+int ltk_fluid_ipc_blob(ltk_fluid *e, char *blob);
+int ltk_fluid_attach_peers(ltk_fluid *e, const char *up_blob, const char *dn_blob);
+/* Same transport between engines of one process (one thread driving several
+ * GPUs, or several slabs on one GPU): peers given directly. */
+int ltk_fluid_attach_peer_engines(ltk_fluid *e, const ltk_fluid *up, const ltk_fluid *dn);
+/* 1 if a peer progress wait ever exceeded its budget (never expected). */
+int ltk_fluid_peer_timeout(ltk_fluid *e, int32_t *timed_out);
 
 /* NCCL (dlopen'ed libnccl.so.2): the 128-byte unique id of rank 0 is
  * broadcast by the caller (torch.distributed) before attach. */

@@ -18,6 +18,7 @@ LIB_PATH = os.path.join(HERE, "_native", "libltk.so")
 Q = 19
 
 LTK_OK = 0
+IPC_BLOB_BYTES = 512
 LTK_ERR_SINGULAR = 11
 MODE_EXACT = 0
 MODE_FAST = 1
@@ -116,6 +117,10 @@ SIGNATURES = {
     "ltk_fluid_run": (ctypes.c_int, [_vp, _i64, _vp]),
     "ltk_fluid_use_graph": (ctypes.c_int, [_vp, _i32]),
     "ltk_fluid_profile": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_float)]),
+    "ltk_fluid_ipc_blob": (ctypes.c_int, [_vp, ctypes.c_char_p]),
+    "ltk_fluid_attach_peers": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p]),
+    "ltk_fluid_attach_peer_engines": (ctypes.c_int, [_vp, _vp, _vp]),
+    "ltk_fluid_peer_timeout": (ctypes.c_int, [_vp, ctypes.POINTER(_i32)]),
     "ltk_nccl_available": (ctypes.c_int, []),
     "ltk_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "ltk_fluid_attach_nccl": (ctypes.c_int, [_vp, ctypes.c_char_p]),

@@ -6,6 +6,7 @@
 // No reference counterpart (reference pkg/README.md:34-35: collision only);
 // specification in DESIGN.md §2-§5.  The collision arithmetic is the
 // reference's (kernels.py:89-125) with the free-energy force terms added.
+#include <cuda.h>  // CUresult / CUdeviceptr for the driver entry point (no libcuda link)
 #include <dlfcn.h>
 #include <nccl.h>  // types only: libnccl.so.2 is dlopen'ed at run time
 
@@ -320,6 +321,19 @@ struct ltk_fluid {
     cudaStream_t st = nullptr, comm_st = nullptr;
     cudaEvent_t ev_fork[3] = {}, ev_join[3] = {};
     ncclComm_t comm = nullptr;
+    // transport between slabs: LOCAL (one slab, periodic images into itself),
+    // NCCL (face exchanges on comm_st), PEER (CUDA IPC: halo images stored by
+    // the kernels straight into the neighbours' buffers over NVLink)
+    int transport = 0;
+    struct Peer {
+        double *fg[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+        double *phi = nullptr, *mu = nullptr;
+        unsigned long long *inbox = nullptr;
+    } up, dn;
+    unsigned long long *inbox = nullptr;  // [2]: progress of the slab below / above
+    int *peer_timeout = nullptr;
+    std::vector<void *> ipc_opened;
+    long long step = 0;  // timesteps taken (lockstep across slabs)
     bool use_graph = false;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool prof = false;
@@ -338,6 +352,8 @@ static void drop_graphs(ltk_fluid *e) {
         }
 }
 
+enum { kLocal = 0, kNccl = 1, kPeer = 2 };
+
 static FluidArgs engine_args(const ltk_fluid *e, int in_state) {
     FluidArgs a;
     fill_args(a, &e->slab, &e->prm);
@@ -352,7 +368,21 @@ static FluidArgs engine_args(const ltk_fluid *e, int in_state) {
     a.mu = e->mu;
     a.mu_out = e->mu;
     a.err = singular_word();
-    a.wrap = (e->nranks == 1 && e->comm == nullptr) ? 1 : 0;
+    if (e->transport == kLocal) {  // periodic images into this slab
+        a.img_f_up = a.img_f_dn = a.f_out;
+        a.img_g_up = a.img_g_dn = a.g_out;
+        a.img_phi_up = a.img_phi_dn = e->phi;
+        a.img_mu_up = a.img_mu_dn = e->mu;
+    } else if (e->transport == kPeer) {  // images into the neighbours over NVLink
+        a.img_f_up = e->up.fg[1 - in_state][0];
+        a.img_g_up = e->up.fg[1 - in_state][1];
+        a.img_f_dn = e->dn.fg[1 - in_state][0];
+        a.img_g_dn = e->dn.fg[1 - in_state][1];
+        a.img_phi_up = e->up.phi;
+        a.img_phi_dn = e->dn.phi;
+        a.img_mu_up = e->up.mu;
+        a.img_mu_dn = e->dn.mu;
+    }
     return a;
 }
 
@@ -402,13 +432,16 @@ static int exchange(ltk_fluid *e, int kind, int s) {
         if (rc_) return rc_;   \
     } while (0)
 
+static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof);
+
 // Enqueue one timestep reading state `s` and writing state 1 - s.
 static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
     FluidArgs a = engine_args(e, s);
     const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
     const long long nzl = e->nzl;
+    if (e->transport == kPeer) return enqueue_step_peer(e, s, st, prof);
     if (prof) cudaEventRecord(e->pev[0], st);
-    if (e->comm == nullptr) {
+    if (e->transport == kLocal) {
         // single slab, periodic z: three kernels, halos written by the kernels
         set_planes(a, vvl, 0, nzl);
         LTK_RC(launch_phi(a, vvl, st));
@@ -469,6 +502,110 @@ static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
     LTK_RC(boundary([&] { return launch_cs(a, vvl, mode, phys, st); }));
     if (prof) cudaEventRecord(e->pev[3], st);
     return LTK_OK;
+}
+
+// ---- peer transport: progress counters pushed into the neighbours' inboxes
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void k_peer_signal(unsigned long long *up_slot, unsigned long long *dn_slot,
+                              unsigned long long v) {
+    __threadfence_system();  // this slab's earlier peer stores before the counter
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(up_slot), "l"(v) : "memory");
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dn_slot), "l"(v) : "memory");
+}
+
+__global__ void k_peer_wait(const unsigned long long *inbox, unsigned long long target,
+                            int *timeout) {
+    long long spins = 0;
+    while (ld_acquire_sys(inbox) < target || ld_acquire_sys(inbox + 1) < target) {
+        if (++spins > (1LL << 28)) {  // never hang the GPU: record and go on
+            atomicExch(timeout, 1);
+            break;
+        }
+        __nanosleep(256);
+    }
+}
+
+static int peer_signal(ltk_fluid *e, unsigned long long v, cudaStream_t st) {
+    // I am the lower neighbour of `up` (its inbox[0]) and the upper one of `dn` (inbox[1])
+    k_peer_signal<<<1, 1, 0, st>>>(e->up.inbox, e->dn.inbox + 1, v);
+    LTK_CHECK_LAUNCH("k_peer_signal");
+    return LTK_OK;
+}
+
+static int peer_wait(ltk_fluid *e, unsigned long long target, cudaStream_t st) {
+    k_peer_wait<<<1, 1, 0, st>>>(e->inbox, target, e->peer_timeout);
+    LTK_CHECK_LAUNCH("k_peer_wait");
+    return LTK_OK;
+}
+
+// One timestep with the peer transport.  Counter protocol per step t:
+// 3t+1 = my f/g images of state t are in place (3t+1 = the load "prime" for
+// t = 0), 3t+2 = phi images sent, 3t+3 = mu images sent, 3t+4 = f/g images of
+// state t+1 sent.  Every wait sits behind the interior planes of a kernel, so
+// the neighbours' progress overlaps local work; the boundary planes then store
+// their halo images straight into the neighbours over NVLink.
+static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
+    FluidArgs a = engine_args(e, s);
+    const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
+    const long long nzl = e->nzl;
+    const unsigned long long t3 = 3ULL * (unsigned long long)e->step;
+    auto ranges = [&](long long lo, long long hi, auto launch_one) -> int {
+        if (hi > lo) {
+            set_planes(a, vvl, lo, hi);
+            return launch_one();
+        }
+        return LTK_OK;
+    };
+    auto boundary = [&](auto launch_one) -> int {
+        LTK_RC(ranges(0, 1, launch_one));
+        if (nzl > 1) LTK_RC(ranges(nzl - 1, nzl, launch_one));
+        return LTK_OK;
+    };
+    auto phi = [&] { return launch_phi(a, vvl, st); };
+    auto mu = [&] { return launch_mu(a, vvl, st); };
+    auto cs = [&] { return launch_cs(a, vvl, mode, phys, st); };
+    if (prof) cudaEventRecord(e->pev[0], st);
+    LTK_RC(ranges(1, nzl - 1, phi));
+    LTK_RC(peer_wait(e, t3 + 1, st));  // f/g halos of state s
+    LTK_RC(boundary(phi));
+    LTK_RC(peer_signal(e, t3 + 2, st));
+    if (prof) cudaEventRecord(e->pev[1], st);
+    if (phys == 1) {
+        LTK_RC(ranges(1, nzl - 1, mu));
+        LTK_RC(peer_wait(e, t3 + 2, st));  // phi halos
+        LTK_RC(boundary(mu));
+    }
+    LTK_RC(peer_signal(e, t3 + 3, st));
+    if (prof) cudaEventRecord(e->pev[2], st);
+    LTK_RC(ranges(1, nzl - 1, cs));
+    LTK_RC(peer_wait(e, t3 + 3, st));  // mu halos
+    LTK_RC(boundary(cs));
+    LTK_RC(peer_signal(e, t3 + 4, st));
+    if (prof) cudaEventRecord(e->pev[3], st);
+    return LTK_OK;
+}
+
+// After a load with the peer transport: push the crossing components of the
+// owned boundary planes of state `s` into the neighbours' halos, then signal.
+static int peer_prime(ltk_fluid *e, int s, cudaStream_t st) {
+    PlaneCopies pc;
+    memset(&pc, 0, sizeof pc);
+    pc.PL = e->nx * e->ny;
+    const ltk_slab *sl = &e->slab;
+    for (int j = 0; j < 5; ++j)
+        for (int d = 0; d < 2; ++d) {
+            pc.src[pc.n] = plane(e->fg[s][d], sl, kUp[j], e->nzl);
+            pc.dst[pc.n++] = plane(e->up.fg[s][d], sl, kUp[j], 0);
+            pc.src[pc.n] = plane(e->fg[s][d], sl, kDown[j], 1);
+            pc.dst[pc.n++] = plane(e->dn.fg[s][d], sl, kDown[j], e->nzl + 1);
+        }
+    LTK_RC(run_plane_copies(pc, st));
+    return peer_signal(e, 3ULL * (unsigned long long)e->step + 1, st);
 }
 
 static int wrap_state_halos(ltk_fluid *e, int s, int which, cudaStream_t st) {
@@ -697,6 +834,16 @@ int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank, in
         ltk_fluid_destroy(e);
         return fail(LTK_ERR_DEVICE, "device error word unavailable");
     }
+    if ((rc = ltk_malloc(&ptr, 2 * sizeof(unsigned long long)))) {
+        ltk_fluid_destroy(e);
+        return rc;
+    }
+    e->inbox = (unsigned long long *)ptr;
+    if ((rc = ltk_malloc(&ptr, sizeof(int)))) {
+        ltk_fluid_destroy(e);
+        return rc;
+    }
+    e->peer_timeout = (int *)ptr;
     *out = e;
     return LTK_OK;
 }
@@ -707,6 +854,9 @@ int ltk_fluid_destroy(ltk_fluid *e) {
     if (e->comm_st) cudaStreamSynchronize(e->comm_st);
     drop_graphs(e);
     if (e->comm && nccl().ok) nccl().CommDestroy(e->comm);
+    for (void *p : e->ipc_opened) cudaIpcCloseMemHandle(p);
+    if (e->inbox) cudaFree(e->inbox);
+    if (e->peer_timeout) cudaFree(e->peer_timeout);
     for (auto &s : e->fg)
         for (auto &p : s)
             if (p) cudaFree(p);
@@ -755,7 +905,8 @@ int ltk_fluid_load(ltk_fluid *e, const double *f_src, const double *g_src, int64
     e->cur = 0;
     LTK_RC(ltk_fluid_scatter(&e->slab, f_src, padded, nz_src, z_src0, Q, e->fg[0][0], st));
     LTK_RC(ltk_fluid_scatter(&e->slab, g_src, padded, nz_src, z_src0, Q, e->fg[0][1], st));
-    if (e->comm == nullptr) LTK_RC(wrap_state_halos(e, 0, 1, st));
+    if (e->transport == kLocal) LTK_RC(wrap_state_halos(e, 0, 1, st));
+    if (e->transport == kPeer) LTK_RC(peer_prime(e, 0, st));
     return LTK_OK;
 }
 
@@ -814,7 +965,7 @@ int ltk_fluid_run(ltk_fluid *e, int64_t nsteps, void *stream) {
             }
             LTK_RC(enqueue_step(e, s, st, true));
             ++e->prof_steps;
-        } else if (e->use_graph && e->comm == nullptr) {
+        } else if (e->use_graph && e->transport == kLocal) {
             if (!e->gexec[s]) {
                 cudaGraph_t g;
                 LTK_CUDA(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
@@ -832,7 +983,130 @@ int ltk_fluid_run(ltk_fluid *e, int64_t nsteps, void *stream) {
             LTK_RC(enqueue_step(e, s, st, false));
         }
         e->cur = 1 - s;
+        ++e->step;
     }
+    return LTK_OK;
+}
+
+// ---- peer transport (CUDA IPC) ----
+// An IPC handle names the whole driver allocation that contains a pointer
+// (small cudaMalloc blocks share one), and the importer gets that
+// allocation's base back; so the blob also carries each buffer's offset from
+// its base (cuMemGetAddressRange, reached through the runtime's driver entry
+// point), and identical handles are opened only once.
+struct IpcBlob {
+    cudaIpcMemHandle_t h[7];  // f0 g0 f1 g1 phi mu inbox
+    unsigned long long off[7];
+};
+static_assert(sizeof(IpcBlob) <= LTK_IPC_BLOB_BYTES, "IPC blob too large");
+
+typedef CUresult (*PfnGetAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+static int alloc_base(void *p, unsigned long long *off) {
+    static PfnGetAddressRange fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *sym = nullptr;
+        LTK_CUDA(cudaGetDriverEntryPoint("cuMemGetAddressRange", &sym, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !sym)
+            return fail(LTK_ERR_DEVICE, "cuMemGetAddressRange unavailable");
+        fn = (PfnGetAddressRange)sym;
+    }
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, (CUdeviceptr)p) != CUDA_SUCCESS)
+        return fail(LTK_ERR_DEVICE, "cuMemGetAddressRange failed");
+    *off = (unsigned long long)((CUdeviceptr)p - base);
+    return LTK_OK;
+}
+
+int ltk_fluid_ipc_blob(ltk_fluid *e, char *blob) {
+    IpcBlob b;
+    void *ptrs[7] = {e->fg[0][0], e->fg[0][1], e->fg[1][0], e->fg[1][1], e->phi, e->mu,
+                     e->inbox};
+    for (int k = 0; k < 7; ++k) {
+        LTK_CUDA(cudaIpcGetMemHandle(&b.h[k], ptrs[k]));
+        LTK_RC(alloc_base(ptrs[k], &b.off[k]));
+    }
+    memset(blob, 0, LTK_IPC_BLOB_BYTES);
+    memcpy(blob, &b, sizeof b);
+    return LTK_OK;
+}
+
+static int open_peer(ltk_fluid *e, const char *blob, ltk_fluid::Peer &p) {
+    IpcBlob b;
+    memcpy(&b, blob, sizeof b);
+    char *ptrs[7];
+    for (int k = 0; k < 7; ++k) {
+        void *base = nullptr;
+        for (int j = 0; j < k; ++j)  // same allocation as an earlier buffer
+            if (memcmp(&b.h[j], &b.h[k], sizeof(cudaIpcMemHandle_t)) == 0)
+                base = ptrs[j] - b.off[j];
+        if (!base) {
+            cudaError_t ce = cudaIpcOpenMemHandle(&base, b.h[k], cudaIpcMemLazyEnablePeerAccess);
+            if (ce != cudaSuccess) return cuda_fail(ce, "cudaIpcOpenMemHandle");
+            e->ipc_opened.push_back(base);
+        }
+        ptrs[k] = (char *)base + b.off[k];
+    }
+    p.fg[0][0] = (double *)ptrs[0];
+    p.fg[0][1] = (double *)ptrs[1];
+    p.fg[1][0] = (double *)ptrs[2];
+    p.fg[1][1] = (double *)ptrs[3];
+    p.phi = (double *)ptrs[4];
+    p.mu = (double *)ptrs[5];
+    p.inbox = (unsigned long long *)ptrs[6];
+    return LTK_OK;
+}
+
+int ltk_fluid_attach_peers(ltk_fluid *e, const char *up_blob, const char *dn_blob) {
+    if (e->nranks < 2) return fail(LTK_ERR_CONFIG, "peer transport needs >= 2 slabs");
+    if (e->transport != kLocal) return fail(LTK_ERR_CONFIG, "transport already attached");
+    LTK_RC(open_peer(e, up_blob, e->up));
+    if (memcmp(up_blob, dn_blob, sizeof(IpcBlob)) == 0)
+        e->dn = e->up;  // two slabs: both neighbours are the same rank
+    else
+        LTK_RC(open_peer(e, dn_blob, e->dn));
+    // complete before returning: the legacy-stream memset must not land after
+    // a neighbour's first progress signal (the caller barriers after attach)
+    LTK_CUDA(cudaMemset(e->inbox, 0, 2 * sizeof(unsigned long long)));
+    LTK_CUDA(cudaMemset(e->peer_timeout, 0, sizeof(int)));
+    LTK_CUDA(cudaStreamSynchronize(0));
+    e->transport = kPeer;
+    drop_graphs(e);
+    return LTK_OK;
+}
+
+static void peer_from_engine(ltk_fluid::Peer &p, const ltk_fluid *o) {
+    for (int st = 0; st < 2; ++st)
+        for (int d = 0; d < 2; ++d) p.fg[st][d] = o->fg[st][d];
+    p.phi = o->phi;
+    p.mu = o->mu;
+    p.inbox = o->inbox;
+}
+
+int ltk_fluid_attach_peer_engines(ltk_fluid *e, const ltk_fluid *up, const ltk_fluid *dn) {
+    if (e->nranks < 2) return fail(LTK_ERR_CONFIG, "peer transport needs >= 2 slabs");
+    if (e->transport != kLocal) return fail(LTK_ERR_CONFIG, "transport already attached");
+    if (up->slab.cstride != e->slab.cstride || dn->slab.cstride != e->slab.cstride)
+        return fail(LTK_ERR_SHAPE, "peer slabs differ in layout");
+    peer_from_engine(e->up, up);
+    peer_from_engine(e->dn, dn);
+    // complete before returning: the legacy-stream memset must not land after
+    // a neighbour's first progress signal (the caller barriers after attach)
+    LTK_CUDA(cudaMemset(e->inbox, 0, 2 * sizeof(unsigned long long)));
+    LTK_CUDA(cudaMemset(e->peer_timeout, 0, sizeof(int)));
+    LTK_CUDA(cudaStreamSynchronize(0));
+    e->transport = kPeer;
+    drop_graphs(e);
+    return LTK_OK;
+}
+
+int ltk_fluid_peer_timeout(ltk_fluid *e, int32_t *timed_out) {
+    LTK_CUDA(cudaStreamSynchronize(e->st));
+    int v = 0;
+    LTK_CUDA(cudaMemcpy(&v, e->peer_timeout, sizeof v, cudaMemcpyDeviceToHost));
+    *timed_out = v;
     return LTK_OK;
 }
 
@@ -851,6 +1125,7 @@ int ltk_fluid_attach_nccl(ltk_fluid *e, const char id[128]) {
     ncclUniqueId u;
     memcpy(u.internal, id, 128);
     LTK_NCCL(nccl().CommInitRank(&e->comm, e->nranks, u, e->rank));
+    e->transport = kNccl;
     drop_graphs(e);
     return LTK_OK;
 }

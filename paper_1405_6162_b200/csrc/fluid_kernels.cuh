@@ -12,9 +12,15 @@
 //   k_mu    mu = A phi + B phi^3 - kappa lap7(phi)               [phi stencil]
 //   k_cs    pull f, g; phi again in registers; grad mu (central);
 //           Guo-forced BGK for f, chemical-potential g_eq; aligned store.
-// With `wrap` set (single slab, periodic z) each kernel also writes the
-// periodic image of its boundary plane into the opposite halo plane, so a
-// one-GPU step needs no halo kernels at all.
+// Halo images: a kernel that produces an owned boundary plane also stores it
+// (phi, mu: the plane; f, g: the components that cross the face) straight into
+// the halo plane that needs it -- the top plane into the bottom halo (zs = 0)
+// of the slab above, the bottom plane into the top halo (zs = nzl+1) of the
+// slab below.  One GPU, periodic z: both targets are this slab's own buffers,
+// so a step needs no halo kernels.  z-slabs over NVLink (peer transport): the
+// targets are the neighbours' buffers mapped with CUDA IPC, so the halo
+// exchange is fused into the producing kernels as peer stores.  NCCL
+// transport: no images (null targets); the engine exchanges faces instead.
 #pragma once
 
 #include "ltk_common.cuh"
@@ -32,7 +38,10 @@ struct FluidArgs {
     double *mu_out;
     long long *err;
     int nx, ny, nzl, z_lo, nplanes;
-    int wrap;             // single slab: also write periodic images into halos
+    // halo image targets (nullptr = none): buffers of the slab above (up) /
+    // below (dn); f/g point at the state being written (f_out/g_out side)
+    double *img_f_up, *img_g_up, *img_f_dn, *img_g_dn;
+    double *img_phi_up, *img_phi_dn, *img_mu_up, *img_mu_dn;
     long long PL, cstride;
     long long nthreads;   // threads of this launch
     long long nz_global, z0;  // for error-site reporting in host order
@@ -96,10 +105,10 @@ __global__ void __launch_bounds__(256) k_phi(const FluidArgs a) {
     });
     const long long off = (long long)p.y * a.nx + p.x0;
     store_vec<VVL>(a.phi_out + (long long)(p.z + 1) * a.PL + off, phi);
-    if (a.wrap) {  // periodic images for the mu stencil
-        if (p.z == 0) store_vec<VVL>(a.phi_out + (long long)(a.nzl + 1) * a.PL + off, phi);
-        if (p.z == a.nzl - 1) store_vec<VVL>(a.phi_out + off, phi);
-    }
+    // halo images for the mu stencil of the neighbouring slabs (or this one)
+    if (p.z == 0 && a.img_phi_dn)
+        store_vec<VVL>(a.img_phi_dn + (long long)(a.nzl + 1) * a.PL + off, phi);
+    if (p.z == a.nzl - 1 && a.img_phi_up) store_vec<VVL>(a.img_phi_up + off, phi);
 }
 
 // ------------------------------------------------------------------ mu
@@ -130,10 +139,9 @@ __global__ void __launch_bounds__(256) k_mu(const FluidArgs a) {
     }
     const long long off = (long long)p.y * a.nx + p.x0;
     store_vec<VVL>(a.mu_out + (long long)(p.z + 1) * a.PL + off, mu);
-    if (a.wrap) {
-        if (p.z == 0) store_vec<VVL>(a.mu_out + (long long)(a.nzl + 1) * a.PL + off, mu);
-        if (p.z == a.nzl - 1) store_vec<VVL>(a.mu_out + off, mu);
-    }
+    if (p.z == 0 && a.img_mu_dn)
+        store_vec<VVL>(a.img_mu_dn + (long long)(a.nzl + 1) * a.PL + off, mu);
+    if (p.z == a.nzl - 1 && a.img_mu_up) store_vec<VVL>(a.img_mu_up + off, mu);
 }
 
 // ------------------------------------------------------------------ collide-stream
@@ -317,20 +325,18 @@ __global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_collide_stream(const 
     static_for<0, Q>([&](auto I) {
         store_vec<VVL>(a.f_out + I.value * a.cstride + o, F[I.value]);
         store_vec<VVL>(a.g_out + I.value * a.cstride + o, G[I.value]);
-        if (a.wrap) {
-            // periodic images of the components that cross the z faces
-            if constexpr (cz(I.value) < 0) {
-                if (p.z == 0) {
-                    const long long h = (long long)(a.nzl + 1) * a.PL + off;
-                    store_vec<VVL>(a.f_out + I.value * a.cstride + h, F[I.value]);
-                    store_vec<VVL>(a.g_out + I.value * a.cstride + h, G[I.value]);
-                }
+        // halo images of the components that cross the z faces
+        if constexpr (cz(I.value) < 0) {
+            if (p.z == 0 && a.img_f_dn) {
+                const long long h = (long long)(a.nzl + 1) * a.PL + off;
+                store_vec<VVL>(a.img_f_dn + I.value * a.cstride + h, F[I.value]);
+                store_vec<VVL>(a.img_g_dn + I.value * a.cstride + h, G[I.value]);
             }
-            if constexpr (cz(I.value) > 0) {
-                if (p.z == a.nzl - 1) {
-                    store_vec<VVL>(a.f_out + I.value * a.cstride + off, F[I.value]);
-                    store_vec<VVL>(a.g_out + I.value * a.cstride + off, G[I.value]);
-                }
+        }
+        if constexpr (cz(I.value) > 0) {
+            if (p.z == a.nzl - 1 && a.img_f_up) {
+                store_vec<VVL>(a.img_f_up + I.value * a.cstride + off, F[I.value]);
+                store_vec<VVL>(a.img_g_up + I.value * a.cstride + off, G[I.value]);
             }
         }
     });

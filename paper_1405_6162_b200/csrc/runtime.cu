@@ -108,8 +108,12 @@ int ltk_malloc(void **ptr, size_t bytes) {
         return fail(LTK_ERR_ALLOC, "cudaMalloc of %zu bytes failed: %s", bytes,
                     cudaGetErrorString(e));
     }
-    // target_malloc zero-initialises (memory.py:231-241)
+    // target_malloc zero-initialises (memory.py:231-241).  cudaMemset runs on
+    // the legacy stream, which does not order against the library's
+    // non-blocking streams: wait for it, or a later copy on another stream
+    // could be overwritten by the late zero fill.
     LTK_CUDA(cudaMemset(*ptr, 0, bytes));
+    LTK_CUDA(cudaStreamSynchronize(0));
     return LTK_OK;
 }
 

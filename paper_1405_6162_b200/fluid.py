@@ -160,6 +160,29 @@ class BinaryFluid:
     def set_graph(self, enable: bool) -> None:
         nat.check(nat.lib.ltk_fluid_use_graph(self._h, 1 if enable else 0), "use_graph")
 
+    def ipc_blob(self) -> bytes:
+        """CUDA IPC handles of this slab's buffers (exchange them, then attach_peers)."""
+        buf = ctypes.create_string_buffer(nat.IPC_BLOB_BYTES)
+        nat.check(nat.lib.ltk_fluid_ipc_blob(self._h, buf), "ltk_fluid_ipc_blob")
+        return buf.raw
+
+    def attach_peers(self, up_blob: bytes, down_blob: bytes) -> None:
+        """Peer transport: halo images are stored by the kernels straight into
+        the slabs above/below over NVLink.  All ranks must attach before any
+        rank loads (put a barrier between the two)."""
+        nat.check(nat.lib.ltk_fluid_attach_peers(self._h, up_blob, down_blob), "attach_peers")
+
+    def attach_peer_engines(self, up: "BinaryFluid", down: "BinaryFluid") -> None:
+        """Peer transport between engines of this process (e.g. one thread
+        driving several GPUs, or several slabs of one GPU)."""
+        nat.check(nat.lib.ltk_fluid_attach_peer_engines(self._h, up.handle, down.handle),
+                  "attach_peer_engines")
+
+    def peer_timed_out(self) -> bool:
+        v = ctypes.c_int32(0)
+        nat.check(nat.lib.ltk_fluid_peer_timeout(self._h, ctypes.byref(v)), "peer_timeout")
+        return bool(v.value)
+
     def attach_nccl(self, unique_id: bytes) -> None:
         if len(unique_id) != 128:
             raise ConfigError("NCCL unique id must be 128 bytes")
