@@ -60,6 +60,9 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=1234)
+    p.add_argument("--transport", choices=("peer", "nccl"), default="peer",
+                   help="N>1 halo exchange: peer stores from the kernels (CUDA IPC over "
+                        "NVLink) or NCCL send/recv")
     return p.parse_args(argv)
 
 
@@ -98,6 +101,16 @@ class Control:
         t = torch.tensor([value], dtype=torch.float64)
         self.dist.all_reduce(t, op=getattr(self.dist.ReduceOp, op))
         return float(t.item())
+
+    def allgather_bytes(self, data: bytes) -> list[bytes]:
+        if not self.dist:
+            return [data]
+        import torch
+
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        out = [torch.zeros_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t)
+        return [bytes(o.numpy().tobytes()) for o in out]
 
     def bcast_bytes(self, data: bytes | None, n: int) -> bytes:
         if not self.dist:
@@ -268,9 +281,13 @@ def run_ours(args, rank, world, local):
     model = lk.D3Q19Model(tau_f=1.0, tau_g=1.0)
     sim = lk.BinaryFluid(shape, model=model, physics="binary", mode=mode, vvl=args.vvl,
                          rank=rank, nranks=world, device=local, use_graph=False)
-    if world > 1:
+    if world > 1 and args.transport == "nccl":
         uid = lk.nccl_unique_id() if rank == 0 else None
         sim.attach_nccl(ctl.bcast_bytes(uid, 128))
+    elif world > 1:
+        blobs = ctl.allgather_bytes(sim.ipc_blob())
+        sim.attach_peers(blobs[(rank + 1) % world], blobs[(rank - 1) % world])
+        ctl.barrier()  # every inbox reset before any neighbour primes it
 
     # per-slab synthetic state in reference order (x*ny + y)*nzl + z
     slab_shape = lk.LatticeShape(nx, ny, nzl)
@@ -351,7 +368,9 @@ def run_ours(args, rank, world, local):
                        "lattice": f"{nx}x{ny}x{nzl * world}", "shape_per_gpu": args.shape,
                        "mode": args.mode, "vvl": args.vvl, "physics": "binary free energy",
                        "l2": "state 10.2 GB/GPU >> 126 MB L2, no flush needed",
-                       "parallelism": f"z-slab x{world}"},
+                       "parallelism": f"z-slab x{world}",
+                       "halo_transport": ("periodic images (one slab)" if world == 1 else
+                                          args.transport)},
             "gpu_launches": launches_all,
             "clocks": clk,
             "roofline": roofline,

@@ -333,7 +333,8 @@ struct ltk_fluid {
     unsigned long long *inbox = nullptr;  // [2]: progress of the slab below / above
     int *peer_timeout = nullptr;
     std::vector<void *> ipc_opened;
-    long long step = 0;  // timesteps taken (lockstep across slabs)
+    long long step = 0;   // timesteps taken (lockstep across slabs)
+    bool primed = false;  // peer transport: halos re-primed by a load since the last step
     bool use_graph = false;
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     bool prof = false;
@@ -543,17 +544,19 @@ static int peer_wait(ltk_fluid *e, unsigned long long target, cudaStream_t st) {
     return LTK_OK;
 }
 
-// One timestep with the peer transport.  Counter protocol per step t:
-// 3t+1 = my f/g images of state t are in place (3t+1 = the load "prime" for
-// t = 0), 3t+2 = phi images sent, 3t+3 = mu images sent, 3t+4 = f/g images of
-// state t+1 sent.  Every wait sits behind the interior planes of a kernel, so
-// the neighbours' progress overlaps local work; the boundary planes then store
-// their halo images straight into the neighbours over NVLink.
+// One timestep with the peer transport.  Counter protocol per step t (each
+// slab pushes its counter into the neighbours' inboxes; waits are ">="):
+//   4t+1  f/g halo images of state t re-primed after a load (peer_prime)
+//   4t+2  phi images sent      4t+3  mu images sent
+//   4t+4  f/g images of state t+1 sent (= "state t+1 ready", 4(t+1))
+// Every wait sits behind the interior planes of a kernel, so the neighbours'
+// progress overlaps local work; the boundary planes then store their halo
+// images straight into the neighbours over NVLink.
 static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
     FluidArgs a = engine_args(e, s);
     const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
     const long long nzl = e->nzl;
-    const unsigned long long t3 = 3ULL * (unsigned long long)e->step;
+    const unsigned long long t4 = 4ULL * (unsigned long long)e->step;
     auto ranges = [&](long long lo, long long hi, auto launch_one) -> int {
         if (hi > lo) {
             set_planes(a, vvl, lo, hi);
@@ -571,27 +574,34 @@ static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
     auto cs = [&] { return launch_cs(a, vvl, mode, phys, st); };
     if (prof) cudaEventRecord(e->pev[0], st);
     LTK_RC(ranges(1, nzl - 1, phi));
-    LTK_RC(peer_wait(e, t3 + 1, st));  // f/g halos of state s
+    LTK_RC(peer_wait(e, t4 + (e->primed ? 1 : 0), st));  // f/g halos of state s
+    e->primed = false;
     LTK_RC(boundary(phi));
-    LTK_RC(peer_signal(e, t3 + 2, st));
+    LTK_RC(peer_signal(e, t4 + 2, st));
     if (prof) cudaEventRecord(e->pev[1], st);
     if (phys == 1) {
         LTK_RC(ranges(1, nzl - 1, mu));
-        LTK_RC(peer_wait(e, t3 + 2, st));  // phi halos
+        LTK_RC(peer_wait(e, t4 + 2, st));  // phi halos
         LTK_RC(boundary(mu));
     }
-    LTK_RC(peer_signal(e, t3 + 3, st));
+    LTK_RC(peer_signal(e, t4 + 3, st));
     if (prof) cudaEventRecord(e->pev[2], st);
     LTK_RC(ranges(1, nzl - 1, cs));
-    LTK_RC(peer_wait(e, t3 + 3, st));  // mu halos
+    LTK_RC(peer_wait(e, t4 + 3, st));  // mu halos
     LTK_RC(boundary(cs));
-    LTK_RC(peer_signal(e, t3 + 4, st));
+    LTK_RC(peer_signal(e, t4 + 4, st));
     if (prof) cudaEventRecord(e->pev[3], st);
     return LTK_OK;
 }
 
-// After a load with the peer transport: push the crossing components of the
-// owned boundary planes of state `s` into the neighbours' halos, then signal.
+// Before a load with the peer transport: the neighbours must have finished
+// the previous step (their reads of the halos we are about to re-prime).
+static int peer_before_load(ltk_fluid *e, cudaStream_t st) {
+    return peer_wait(e, 4ULL * (unsigned long long)e->step, st);
+}
+
+// After the load: push the crossing components of the owned boundary planes
+// of state `s` into the neighbours' halos, then signal 4t+1.
 static int peer_prime(ltk_fluid *e, int s, cudaStream_t st) {
     PlaneCopies pc;
     memset(&pc, 0, sizeof pc);
@@ -605,7 +615,51 @@ static int peer_prime(ltk_fluid *e, int s, cudaStream_t st) {
             pc.dst[pc.n++] = plane(e->dn.fg[s][d], sl, kDown[j], e->nzl + 1);
         }
     LTK_RC(run_plane_copies(pc, st));
-    return peer_signal(e, 3ULL * (unsigned long long)e->step + 1, st);
+    e->primed = true;
+    return peer_signal(e, 4ULL * (unsigned long long)e->step + 1, st);
+}
+
+// Load every kernel a step can launch.  With lazy module loading (the CUDA 12
+// default) the first launch of a kernel loads its module, which waits for the
+// device to go idle; with the peer transport a progress-wait kernel may be
+// spinning on a neighbour whose work is not enqueued yet, so a lazy load in
+// the middle of an enqueue would stall until the spin budget runs out.
+template <int MODE, int PHYS>
+static void preload_cs(cudaFuncAttributes &fa) {
+    cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 0>);
+    cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, 0>);
+    if (MODE == LTK_MODE_EXACT) {
+        cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 1>);
+        cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 2>);
+        cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 3>);
+        cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, 1>);
+        cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, 2>);
+        cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, 3>);
+    }
+}
+
+static int preload_step_kernels() {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_phi<1>);
+    cudaFuncGetAttributes(&fa, k_phi<2>);
+    cudaFuncGetAttributes(&fa, k_phi<4>);
+    cudaFuncGetAttributes(&fa, k_mu<1>);
+    cudaFuncGetAttributes(&fa, k_mu<2>);
+    cudaFuncGetAttributes(&fa, k_mu<4>);
+    cudaFuncGetAttributes(&fa, k_mu_tma);
+    cudaFuncGetAttributes(&fa, k_plane_copy);
+    cudaFuncGetAttributes(&fa, k_peer_wait);
+    cudaFuncGetAttributes(&fa, k_peer_signal);
+    cudaFuncGetAttributes(&fa, k_transpose<true>);
+    cudaFuncGetAttributes(&fa, k_transpose<false>);
+    preload_cs<LTK_MODE_EXACT, 0>(fa);
+    preload_cs<LTK_MODE_EXACT, 1>(fa);
+    preload_cs<LTK_MODE_FAST, 0>(fa);
+    preload_cs<LTK_MODE_FAST, 1>(fa);
+    LTK_CUDA(cudaFuncSetAttribute(k_mu_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(200 * 1024)));
+    LTK_CUDA(cudaGetLastError());
+    return LTK_OK;
 }
 
 static int wrap_state_halos(ltk_fluid *e, int s, int which, cudaStream_t st) {
@@ -902,6 +956,7 @@ int ltk_fluid_set_params(ltk_fluid *e, const ltk_fluid_params *p) {
 int ltk_fluid_load(ltk_fluid *e, const double *f_src, const double *g_src, int64_t padded,
                    int64_t nz_src, int64_t z_src0, void *stream) {
     cudaStream_t st = stream ? as_stream(stream) : e->st;
+    if (e->transport == kPeer) LTK_RC(peer_before_load(e, st));
     e->cur = 0;
     LTK_RC(ltk_fluid_scatter(&e->slab, f_src, padded, nz_src, z_src0, Q, e->fg[0][0], st));
     LTK_RC(ltk_fluid_scatter(&e->slab, g_src, padded, nz_src, z_src0, Q, e->fg[0][1], st));
@@ -1062,6 +1117,7 @@ static int open_peer(ltk_fluid *e, const char *blob, ltk_fluid::Peer &p) {
 int ltk_fluid_attach_peers(ltk_fluid *e, const char *up_blob, const char *dn_blob) {
     if (e->nranks < 2) return fail(LTK_ERR_CONFIG, "peer transport needs >= 2 slabs");
     if (e->transport != kLocal) return fail(LTK_ERR_CONFIG, "transport already attached");
+    LTK_RC(preload_step_kernels());
     LTK_RC(open_peer(e, up_blob, e->up));
     if (memcmp(up_blob, dn_blob, sizeof(IpcBlob)) == 0)
         e->dn = e->up;  // two slabs: both neighbours are the same rank
@@ -1090,6 +1146,7 @@ int ltk_fluid_attach_peer_engines(ltk_fluid *e, const ltk_fluid *up, const ltk_f
     if (e->transport != kLocal) return fail(LTK_ERR_CONFIG, "transport already attached");
     if (up->slab.cstride != e->slab.cstride || dn->slab.cstride != e->slab.cstride)
         return fail(LTK_ERR_SHAPE, "peer slabs differ in layout");
+    LTK_RC(preload_step_kernels());
     peer_from_engine(e->up, up);
     peer_from_engine(e->dn, dn);
     // complete before returning: the legacy-stream memset must not land after

@@ -105,6 +105,12 @@ def test_engines_in_one_process_bitwise(nslabs, physics):
     try:
         for r, sim in enumerate(sims):
             sim.attach_peer_engines(sims[(r + 1) % nslabs], sims[(r - 1) % nslabs])
+        # a first state, one step, then a re-load: the halos must be re-primed
+        fa, ga = random_binary_state(full, np.random.default_rng(7), model)
+        for sim in sims:
+            sim.load(fa, ga)
+        for sim in sims:
+            sim.run(1)
         f0, g0 = random_binary_state(full, np.random.default_rng(31), model)
         for sim in sims:
             sim.load(f0, g0)
