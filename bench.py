@@ -53,7 +53,12 @@ def parse_args(argv=None):
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--shape", default="256x256x256", help="per-GPU lattice NXxNYxNZ")
+    p.add_argument("--shape", default=None,
+                   help="lattice NXxNYxNZ: per GPU for --scaling weak (default 256^3), "
+                        "global for --scaling strong (default 512^3)")
+    p.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                   help="weak: BASELINE configs[2]/[4], 256^3 per GPU; strong: configs[3], "
+                        "one global lattice split into z-slabs")
     p.add_argument("--mode", choices=("exact", "fast"), default="fast")
     p.add_argument("--vvl", type=int, default=1)
     p.add_argument("--e2e-steps", type=int, default=4)
@@ -275,7 +280,13 @@ def run_ours(args, rank, world, local):
 
     ctl = Control(world)
     nat.check(nat.lib.ltk_set_device(local))
-    nx, ny, nzl = (int(v) for v in args.shape.lower().split("x"))
+    nx, ny, nz_arg = (int(v) for v in args.shape.lower().split("x"))
+    if args.scaling == "strong":
+        if nz_arg % world:
+            raise SystemExit(f"nz {nz_arg} not divisible by {world} GPUs")
+        nzl = nz_arg // world
+    else:
+        nzl = nz_arg
     shape = lk.LatticeShape(nx, ny, nzl * world)
     mode = lk.MODE_FAST if args.mode == "fast" else lk.MODE_EXACT
     model = lk.D3Q19Model(tau_f=1.0, tau_g=1.0)
@@ -341,7 +352,7 @@ def run_ours(args, rank, world, local):
 
     # ---------------- e2e: public API with host buffers, every step
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.scaling == "weak":  # strong: 41 GB of state per 512^3 GPU
         e2e = run_e2e(args, sim, f0, g0, ctl, world, nat, lk)
 
     # ---------------- CPU baseline (rank 0, N=1)
@@ -359,15 +370,20 @@ def run_ours(args, rank, world, local):
             "metric": "lattice site updates/sec (MLUPS), D3Q19 binary-fluid full timestep",
             "value": value, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "full timestep (stream + phi + mu + forced collision), "
-                                   f"{args.shape} per GPU, z-slabs" +
-                                   (" (BASELINE configs[2])" if world == 1 else
-                                    " (BASELINE configs[4], weak scaling)"),
-                       "lattice": f"{nx}x{ny}x{nzl * world}", "shape_per_gpu": args.shape,
+            "config": {"workload": "full timestep (stream + phi + mu + forced collision), " +
+                                   (f"{args.shape} per GPU, z-slabs" +
+                                    (" (BASELINE configs[2])" if world == 1 else
+                                     " (BASELINE configs[4], weak scaling)")
+                                    if args.scaling == "weak" else
+                                    f"{args.shape} global lattice in {world} z-slabs "
+                                    "(BASELINE configs[3], strong scaling)"),
+                       "lattice": f"{nx}x{ny}x{nzl * world}",
+                       "shape_per_gpu": f"{nx}x{ny}x{nzl}",
                        "mode": args.mode, "vvl": args.vvl, "physics": "binary free energy",
-                       "l2": "state 10.2 GB/GPU >> 126 MB L2, no flush needed",
+                       "l2": f"state {4 * 19 * 8 * nx * ny * nzl / 1e9:.1f} GB/GPU >> 126 MB L2, "
+                             "no flush needed",
                        "parallelism": f"z-slab x{world}",
                        "halo_transport": ("periodic images (one slab)" if world == 1 else
                                           args.transport)},
@@ -462,6 +478,8 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
 
 def main(argv=None):
     args = parse_args(argv)
+    if args.shape is None:
+        args.shape = "512x512x512" if args.scaling == "strong" else "256x256x256"
     rank, world, local = dist_env()
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)

@@ -100,15 +100,20 @@ static int launch_mu(const FluidArgs &a, int vvl, cudaStream_t st) {
     if (mu_tma_ok(a)) {
         // shared-memory staged stencil, rows loaded by TMA bulk copies
         static bool attr_set = false;
-        const size_t smem = mu_tma_smem(a);
-        if (!attr_set || smem > 48 * 1024) {
-            LTK_CUDA(cudaFuncSetAttribute(k_mu_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (!attr_set) {
+            LTK_CUDA(cudaFuncSetAttribute(k_mu_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)(200 * 1024)));
+            LTK_CUDA(cudaFuncSetAttribute(k_mu_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)(200 * 1024)));
             attr_set = true;
         }
-        dim3 grid((unsigned)(a.ny / kMuTY), (unsigned)((a.nplanes + kMuZ - 1) / kMuZ));
+        const int rows = mu_tma_rows(a.nx);
+        dim3 grid((unsigned)(a.ny / rows), (unsigned)((a.nplanes + kMuZ - 1) / kMuZ));
         const int threads = std::min(256, (a.nx + 31) / 32 * 32);
-        k_mu_tma<<<grid, threads, smem, st>>>(a);
+        if (rows == 4)
+            k_mu_tma<4><<<grid, threads, mu_tma_smem(a), st>>>(a);
+        else
+            k_mu_tma<2><<<grid, threads, mu_tma_smem(a), st>>>(a);
         LTK_CHECK_LAUNCH("k_mu_tma");
         return LTK_OK;
     }
@@ -646,7 +651,8 @@ static int preload_step_kernels() {
     cudaFuncGetAttributes(&fa, k_mu<1>);
     cudaFuncGetAttributes(&fa, k_mu<2>);
     cudaFuncGetAttributes(&fa, k_mu<4>);
-    cudaFuncGetAttributes(&fa, k_mu_tma);
+    cudaFuncGetAttributes(&fa, k_mu_tma<4>);
+    cudaFuncGetAttributes(&fa, k_mu_tma<2>);
     cudaFuncGetAttributes(&fa, k_plane_copy);
     cudaFuncGetAttributes(&fa, k_peer_wait);
     cudaFuncGetAttributes(&fa, k_peer_signal);
@@ -656,7 +662,9 @@ static int preload_step_kernels() {
     preload_cs<LTK_MODE_EXACT, 1>(fa);
     preload_cs<LTK_MODE_FAST, 0>(fa);
     preload_cs<LTK_MODE_FAST, 1>(fa);
-    LTK_CUDA(cudaFuncSetAttribute(k_mu_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    LTK_CUDA(cudaFuncSetAttribute(k_mu_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)(200 * 1024)));
+    LTK_CUDA(cudaFuncSetAttribute(k_mu_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(200 * 1024)));
     LTK_CUDA(cudaGetLastError());
     return LTK_OK;

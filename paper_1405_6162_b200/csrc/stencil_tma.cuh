@@ -19,9 +19,12 @@ namespace ltk {
 // Measured on the B200 at 256^3 (k_mu time per step): TY 8 / 4 slots 0.096 ms,
 // TY 4 / 6 slots 0.071 ms, TY 4 / 8 slots 0.084 ms, TY 2 / 8 slots 0.080 ms;
 // the unstaged k_mu took 0.107 ms.
-constexpr int kMuTY = 4;     // rows per CTA
+// Rows per CTA: 4 up to nx = 256, 2 beyond (keeps a CTA's ring <= ~75 KB so
+// three CTAs share an SM).
 constexpr int kMuZ = 16;     // planes per CTA
 constexpr int kMuSlots = 6;  // plane ring: planes z-1..z+1 in use, 3 in flight
+
+inline int mu_tma_rows(int nx) { return nx <= 256 ? 4 : 2; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -59,6 +62,7 @@ __device__ __forceinline__ void tma_row(void *dst, const void *src, uint32_t byt
 }
 
 // Issue the TY+2 row copies of storage plane zs into ring slot `slot`.
+template <int kMuTY>
 __device__ __forceinline__ void load_plane(double *ring, uint64_t *bars, int slot, const FluidArgs &a,
                                            int y0, int zs) {
     const int nx = a.nx;
@@ -73,6 +77,7 @@ __device__ __forceinline__ void load_plane(double *ring, uint64_t *bars, int slo
 }
 
 // grid: (ny / kMuTY, ceil(nplanes / kMuZ)); block: up to 256 threads over x.
+template <int kMuTY>
 __global__ void __launch_bounds__(256) k_mu_tma(const FluidArgs a) {
     extern __shared__ __align__(128) double ring[];
     __shared__ __align__(8) uint64_t bars[kMuSlots];
@@ -89,7 +94,7 @@ __global__ void __launch_bounds__(256) k_mu_tma(const FluidArgs a) {
     const int first = zb - 1, last = ze;
     if (threadIdx.x == 0)
         for (int z = first; z <= min(last, first + kMuSlots - 1); ++z)
-            load_plane(ring, bars, (z - first) % kMuSlots, a, y0, z + 1);
+            load_plane<kMuTY>(ring, bars, (z - first) % kMuSlots, a, y0, z + 1);
     const size_t slot_elems = (size_t)(kMuTY + 2) * nx;
     for (int z = zb; z < ze; ++z) {
         const int sm = (z - 1 - first) % kMuSlots, s0 = (z - first) % kMuSlots,
@@ -125,18 +130,17 @@ __global__ void __launch_bounds__(256) k_mu_tma(const FluidArgs a) {
         const int nz_next = z - 1 + kMuSlots;  // plane that reuses slot sm
         if (threadIdx.x == 0 && nz_next <= last) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            load_plane(ring, bars, sm, a, y0, nz_next + 1);
+            load_plane<kMuTY>(ring, bars, sm, a, y0, nz_next + 1);
         }
     }
 }
 
-inline bool mu_tma_ok(const FluidArgs &a) {
-    return a.ny % kMuTY == 0 && a.nx % 2 == 0 && (size_t)kMuSlots * (kMuTY + 2) * a.nx * 8 <=
-                                                       200 * 1024;
+inline size_t mu_tma_smem(const FluidArgs &a) {
+    return (size_t)kMuSlots * (mu_tma_rows(a.nx) + 2) * a.nx * 8;
 }
 
-inline size_t mu_tma_smem(const FluidArgs &a) {
-    return (size_t)kMuSlots * (kMuTY + 2) * a.nx * 8;
+inline bool mu_tma_ok(const FluidArgs &a) {
+    return a.ny % mu_tma_rows(a.nx) == 0 && a.nx % 2 == 0 && mu_tma_smem(a) <= 200 * 1024;
 }
 
 }  // namespace ltk
