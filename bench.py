@@ -61,7 +61,7 @@ def parse_args(argv=None):
                         "one global lattice split into z-slabs")
     p.add_argument("--mode", choices=("exact", "fast"), default="fast")
     p.add_argument("--vvl", type=int, default=1)
-    p.add_argument("--e2e-steps", type=int, default=4)
+    p.add_argument("--e2e-steps", type=int, default=16)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=1234)
