@@ -306,7 +306,7 @@ def run_ours(args, rank, world, local):
     sim.load(f0, g0)
     sites_rank = nx * ny * nzl
 
-    launches0 = nat.launch_count()
+    tot0 = [ctl.allreduce(float(v), "SUM") for v in sim.totals()]  # whole lattice
     sim.run(args.warmup)
     sim.sync()
     ctl.barrier()
@@ -325,6 +325,7 @@ def run_ours(args, rank, world, local):
     sim.sync()
     prof = sim.profile(False)
     ms = nat.elapsed_ms(start, stop)
+    tot1 = [ctl.allreduce(float(v), "SUM") for v in sim.totals()]
     launches = nat.launch_count() - l_before
     ctl.barrier()
     clk = clocks.stop() if rank == 0 else None
@@ -388,6 +389,11 @@ def run_ours(args, rank, world, local):
                        "halo_transport": ("periodic images (one slab)" if world == 1 else
                                           args.transport)},
             "gpu_launches": launches_all,
+            "conservation": {"steps": args.warmup + args.steps,
+                             "mass_rel_drift": abs(tot1[0] - tot0[0]) / abs(tot0[0]),
+                             "phi_rel_drift": abs(tot1[4] - tot0[4]) / abs(tot0[4]),
+                             "note": "whole lattice, totals summed over ranks "
+                                     "(ltk_fluid_totals)"},
             "clocks": clk,
             "roofline": roofline,
             "cpu_baseline": cpu,
@@ -468,6 +474,10 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
         nat.free(p)
     for s in (h2d_st, d2h_st):
         L.ltk_stream_destroy(s)
+    from paper_1405_6162_b200.memory import pinned_free
+
+    for arr in (hf, hg, of, og):
+        pinned_free(arr)
     sites = sim.shape.nx * sim.shape.ny * nzl * world
     return {"value": sites * args.e2e_steps / (ms_max * 1e-3) / 1e6, "unit": "MLUPS",
             "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,

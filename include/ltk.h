@@ -227,6 +227,10 @@ int ltk_fluid_load(ltk_fluid *e, const double *f_src, const double *g_src, int64
                    int64_t nz_src, int64_t z_src0, void *stream);
 int ltk_fluid_store(ltk_fluid *e, double *f_dst, double *g_dst, int64_t padded,
                     int64_t nz_src, int64_t z_src0, void *stream);
+/* Diagnostics of the current state over this slab's owned sites:
+ * out5 = {sum rho, sum j_x, sum j_y, sum j_z, sum phi} (synchronous;
+ * deterministic block-tree order; sum over slabs for the whole lattice). */
+int ltk_fluid_totals(ltk_fluid *e, double *out5);
 /* Run n full timesteps on the engine stream (or `stream` if not NULL). */
 int ltk_fluid_run(ltk_fluid *e, int64_t nsteps, void *stream);
 /* Capture one step pair (A->B, B->A) into CUDA graphs used by ltk_fluid_run. */

@@ -510,6 +510,39 @@ static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
     return LTK_OK;
 }
 
+// ---- diagnostics: totals of rho, momentum, phi over the owned sites
+// Block partial sums in a fixed tree, summed on the host in block order:
+// deterministic for a given lattice (not the numpy summation order).
+constexpr int kTotBlocks = 592, kTotThreads = 256;
+
+__global__ void __launch_bounds__(kTotThreads) k_totals(const double *f, const double *g,
+                                                        long long nx, long long ny, long long nzl,
+                                                        long long cstride, double *partial) {
+    const long long PL = nx * ny, n = PL * nzl;
+    double acc[5] = {0, 0, 0, 0, 0};
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long o = PL + t;  // storage plane 1 onwards
+        static_for<0, Q>([&](auto I) {
+            const double fi = f[I.value * cstride + o];
+            acc[0] += fi;
+            if constexpr (cx(I.value) != 0) acc[1] += cx(I.value) * fi;
+            if constexpr (cy(I.value) != 0) acc[2] += cy(I.value) * fi;
+            if constexpr (cz(I.value) != 0) acc[3] += cz(I.value) * fi;
+            acc[4] += g[I.value * cstride + o];
+        });
+    }
+    __shared__ double red[5][kTotThreads];
+    for (int k = 0; k < 5; ++k) red[k][threadIdx.x] = acc[k];
+    __syncthreads();
+    for (int w = kTotThreads / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w)
+            for (int k = 0; k < 5; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x < 5) partial[blockIdx.x * 5 + threadIdx.x] = red[threadIdx.x][0];
+}
+
 // ---- peer transport: progress counters pushed into the neighbours' inboxes
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
@@ -978,6 +1011,23 @@ int ltk_fluid_store(ltk_fluid *e, double *f_dst, double *g_dst, int64_t padded, 
     cudaStream_t st = stream ? as_stream(stream) : e->st;
     LTK_RC(ltk_fluid_gather(&e->slab, e->fg[e->cur][0], padded, nz_src, z_src0, Q, f_dst, st));
     LTK_RC(ltk_fluid_gather(&e->slab, e->fg[e->cur][1], padded, nz_src, z_src0, Q, g_dst, st));
+    return LTK_OK;
+}
+
+int ltk_fluid_totals(ltk_fluid *e, double *out5) {
+    double *partial = nullptr;
+    LTK_CUDA(cudaMallocAsync(&partial, sizeof(double) * 5 * kTotBlocks, e->st));
+    k_totals<<<kTotBlocks, kTotThreads, 0, e->st>>>(e->fg[e->cur][0], e->fg[e->cur][1], e->nx,
+                                                   e->ny, e->nzl, e->slab.cstride, partial);
+    LTK_CHECK_LAUNCH("k_totals");
+    std::vector<double> h(5 * kTotBlocks);
+    LTK_CUDA(cudaMemcpyAsync(h.data(), partial, sizeof(double) * h.size(),
+                             cudaMemcpyDeviceToHost, e->st));
+    LTK_CUDA(cudaFreeAsync(partial, e->st));
+    LTK_CUDA(cudaStreamSynchronize(e->st));
+    for (int k = 0; k < 5; ++k) out5[k] = 0.0;
+    for (int b = 0; b < kTotBlocks; ++b)
+        for (int k = 0; k < 5; ++k) out5[k] += h[b * 5 + k];
     return LTK_OK;
 }
 

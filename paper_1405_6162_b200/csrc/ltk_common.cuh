@@ -13,7 +13,6 @@
 namespace ltk {
 
 // ---------------------------------------------------------------- errors
-void set_error(const char *fmt, ...);
 int fail(int status, const char *fmt, ...);
 int cuda_fail(cudaError_t err, const char *what);
 void count_launch(int n = 1);
@@ -124,11 +123,6 @@ struct Fast {
 };
 
 // Vector load/store of VVL consecutive doubles (VVL*8-byte aligned).
-template <int VVL>
-struct Vec {
-    double v[VVL];
-};
-
 template <int VVL>
 __device__ __forceinline__ void load_vec(double (&dst)[VVL], const double *p) {
     if constexpr (VVL == 1) {

@@ -17,13 +17,6 @@ namespace ltk {
 static thread_local char g_msg[512] = "";
 static std::atomic<long long> g_launches{0};
 
-void set_error(const char *fmt, ...) {
-    va_list ap;
-    va_start(ap, fmt);
-    vsnprintf(g_msg, sizeof g_msg, fmt, ap);
-    va_end(ap);
-}
-
 int fail(int status, const char *fmt, ...) {
     va_list ap;
     va_start(ap, fmt);

@@ -267,6 +267,15 @@ class BinaryFluid:
         self.sync()
         return tuple(a[PL:(self.nzl + 1) * PL].reshape(self.nzl, s.ny, s.nx) for a in out)
 
+    def totals(self, allreduce=None) -> np.ndarray:
+        """[sum rho, sum j_x, sum j_y, sum j_z, sum phi] of the current state on
+        the device (no state copy).  `allreduce(np.ndarray) -> np.ndarray`
+        sums the slabs of a multi-GPU run (e.g. torch.distributed)."""
+        out = (ctypes.c_double * 5)()
+        nat.check(nat.lib.ltk_fluid_totals(self._h, out), "ltk_fluid_totals")
+        tot = np.array(out[:])
+        return allreduce(tot) if allreduce is not None else tot
+
     # -- stepping ------------------------------------------------------------
 
     def run(self, nsteps: int, stream: int | None = None) -> None:

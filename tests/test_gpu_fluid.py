@@ -193,6 +193,24 @@ class TestFullSizeProperties:
         assert abs(p1 - p0) <= 1e-10 * abs(p0)
         assert np.all(np.isfinite(f1.data)) and np.all(np.isfinite(g1.data))
 
+    def test_totals_match_fields(self, lk):
+        shape = lk.LatticeShape(64, 32, 48)
+        f0, g0 = _state(lk, (64, 32, 48), 4)
+        with lk.BinaryFluid(shape, mode=lk.MODE_FAST) as sim:
+            sim.load(f0, g0)
+            t0 = sim.totals()
+            sim.run(10)
+            t1 = sim.totals()
+            f1, g1 = sim.fields()
+        n, P = shape.nsites, f0.descriptor.padded_sites
+        fc = f1.data.reshape(19, P)[:, :n]
+        cv = lk.D3Q19Model().cvf
+        ref = [fc.sum(), (cv[:, 0] @ fc).sum(), (cv[:, 1] @ fc).sum(), (cv[:, 2] @ fc).sum(),
+               g1.data.reshape(19, P)[:, :n].sum()]
+        assert np.allclose(t1, ref, rtol=1e-12, atol=1e-9)
+        assert abs(t1[0] - t0[0]) <= 1e-12 * t0[0]      # mass conserved
+        assert abs(t1[4] - t0[4]) <= 1e-12 * abs(t0[4])  # phi conserved
+
     def test_ragged_shapes(self, lk):
         # odd extents, nx not a multiple of the warp, planes of odd size
         for shape in ((7, 6, 5), (33, 10, 3), (2, 2, 2), (64, 3, 9)):
