@@ -666,7 +666,7 @@ template <int MODE, int PHYS>
 static void preload_cs(cudaFuncAttributes &fa) {
     cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 0>);
     cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, 0>);
-    if (MODE == LTK_MODE_EXACT) {
+    if constexpr (MODE == LTK_MODE_EXACT) {
         cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 1>);
         cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 2>);
         cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 3>);

@@ -106,9 +106,16 @@ __global__ void __launch_bounds__(256) k_phi(const FluidArgs a) {
     const long long off = (long long)p.y * a.nx + p.x0;
     store_vec<VVL>(a.phi_out + (long long)(p.z + 1) * a.PL + off, phi);
     // halo images for the mu stencil of the neighbouring slabs (or this one)
-    if (p.z == 0 && a.img_phi_dn)
+    bool img = false;
+    if (p.z == 0 && a.img_phi_dn) {
         store_vec<VVL>(a.img_phi_dn + (long long)(a.nzl + 1) * a.PL + off, phi);
-    if (p.z == a.nzl - 1 && a.img_phi_up) store_vec<VVL>(a.img_phi_up + off, phi);
+        img = true;
+    }
+    if (p.z == a.nzl - 1 && a.img_phi_up) {
+        store_vec<VVL>(a.img_phi_up + off, phi);
+        img = true;
+    }
+    if (img) __threadfence_system();  // peer images visible before the progress signal
 }
 
 // ------------------------------------------------------------------ mu
@@ -139,9 +146,16 @@ __global__ void __launch_bounds__(256) k_mu(const FluidArgs a) {
     }
     const long long off = (long long)p.y * a.nx + p.x0;
     store_vec<VVL>(a.mu_out + (long long)(p.z + 1) * a.PL + off, mu);
-    if (p.z == 0 && a.img_mu_dn)
+    bool img = false;
+    if (p.z == 0 && a.img_mu_dn) {
         store_vec<VVL>(a.img_mu_dn + (long long)(a.nzl + 1) * a.PL + off, mu);
-    if (p.z == a.nzl - 1 && a.img_mu_up) store_vec<VVL>(a.img_mu_up + off, mu);
+        img = true;
+    }
+    if (p.z == a.nzl - 1 && a.img_mu_up) {
+        store_vec<VVL>(a.img_mu_up + off, mu);
+        img = true;
+    }
+    if (img) __threadfence_system();
 }
 
 // ------------------------------------------------------------------ collide-stream
@@ -340,6 +354,8 @@ __global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_collide_stream(const 
             }
         }
     });
+    if ((p.z == 0 && a.img_f_dn) || (p.z == a.nzl - 1 && a.img_f_up))
+        __threadfence_system();  // peer images visible before the progress signal
 }
 
 }  // namespace ltk

@@ -122,8 +122,14 @@ __global__ void __launch_bounds__(256) k_mu_tma(const FluidArgs a) {
                                             __dmul_rn(a.kappa, lap));
                 const long long off = (long long)y * nx + x;
                 a.mu_out[(long long)(z + 1) * a.PL + off] = mu;
-                if (z == 0 && a.img_mu_dn) a.img_mu_dn[(long long)(a.nzl + 1) * a.PL + off] = mu;
-                if (z == a.nzl - 1 && a.img_mu_up) a.img_mu_up[off] = mu;
+                if (z == 0 && a.img_mu_dn) {
+                    a.img_mu_dn[(long long)(a.nzl + 1) * a.PL + off] = mu;
+                    __threadfence_system();
+                }
+                if (z == a.nzl - 1 && a.img_mu_up) {
+                    a.img_mu_up[off] = mu;
+                    __threadfence_system();
+                }
             }
         }
         __syncthreads();  // every thread is done with plane z-1's slot
