@@ -40,10 +40,22 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-#: algorithmic bytes per site update: read f,g 2*19*8 + mu 8, write f,g 2*19*8
+#: algorithmic HBM bytes per site update.  k_collide_stream:
+#: read f,g 2*19*8 + mu 8, write f,g 2*19*8.  k_cs_phi (fused, default) adds the
+#: next state's phi write (8); its re-read of g' is served by L2, not HBM.
 CS_BYTES_PER_SITE = 616
-#: whole step: phi (read g 152 + write 8) + mu (read 8 + write 8) + collide-stream 616
+CSPHI_BYTES_PER_SITE = 624
+#: whole step, three kernels: phi (read g 152 + write 8) + mu (read 8 + write 8) + 616
 STEP_BYTES_PER_SITE = 792
+PHI_BYTES_PER_SITE, MU_BYTES_PER_SITE = 160, 16
+
+
+def step_bytes_per_site(fused: bool, nzl: int) -> float:
+    """Algorithmic bytes of one step per site: fused, k_phi runs on the 2
+    boundary planes only."""
+    if not fused:
+        return STEP_BYTES_PER_SITE
+    return CSPHI_BYTES_PER_SITE + MU_BYTES_PER_SITE + PHI_BYTES_PER_SITE * 2.0 / nzl
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -65,6 +77,11 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=1234)
+    p.add_argument("--fuse", action="store_true",
+                   help="k_cs_phi (collide-stream + next-state phi) instead of the "
+                        "three-kernel step")
+    p.add_argument("--fuse-lag", type=int, default=1,
+                   help="planes of slack between the collision and phi fronts of k_cs_phi")
     p.add_argument("--transport", choices=("peer", "nccl"), default="peer",
                    help="N>1 halo exchange: peer stores from the kernels (CUDA IPC over "
                         "NVLink) or NCCL send/recv")
@@ -197,14 +214,14 @@ def measured_hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(shape: str, mode: str, world: int):
-    """dram_bytes_read+write per k_collide_stream launch for this config, from
-    the committed ncu capture (profiles/ncu_traffic.json); None if not captured."""
+def ncu_traffic(shape: str, mode: str, world: int, kernel: str = "k_collide_stream"):
+    """dram_bytes_read+write per launch of `kernel` for this config, from the
+    committed ncu capture (profiles/ncu_traffic.json); None if not captured."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as fh:
             data = json.load(fh)
-        return data.get(f"{shape}/{mode}/p{world}", {}).get("k_collide_stream_dram_bytes")
+        return data.get(f"{shape}/{mode}/p{world}", {}).get(f"{kernel}_dram_bytes")
     except Exception:
         return None
 
@@ -292,6 +309,8 @@ def run_ours(args, rank, world, local):
     model = lk.D3Q19Model(tau_f=1.0, tau_g=1.0)
     sim = lk.BinaryFluid(shape, model=model, physics="binary", mode=mode, vvl=args.vvl,
                          rank=rank, nranks=world, device=local, use_graph=False)
+    fused = args.fuse
+    sim.set_fuse(fused, args.fuse_lag)
     if world > 1 and args.transport == "nccl":
         uid = lk.nccl_unique_id() if rank == 0 else None
         sim.attach_nccl(ctl.bcast_bytes(uid, 128))
@@ -335,21 +354,24 @@ def run_ours(args, rank, world, local):
     total_sites = sites_rank * world
     value = total_sites * args.steps / (ms_max * 1e-3) / 1e6  # MLUPS
 
-    # dominant kernel: k_collide_stream (all planes) -- prof[2] covers it
+    # dominant kernel: k_cs_phi (fused) or k_collide_stream, all planes -- prof[2] covers it
     cs_ms = prof[2] / args.steps
     peak, peak_src = measured_hbm_peak()
-    achieved = CS_BYTES_PER_SITE * sites_rank / (cs_ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.shape, args.mode, world)
-    roofline = {"bound": "hbm", "kernel": "k_collide_stream", "achieved": achieved,
+    kname = "k_cs_phi" if fused else "k_collide_stream"
+    cs_bytes = CSPHI_BYTES_PER_SITE if fused else CS_BYTES_PER_SITE
+    achieved = cs_bytes * sites_rank / (cs_ms * 1e-3) / 1e9
+    traffic = ncu_traffic(args.shape, args.mode, world, kname)
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src,
-                "bytes_per_site": CS_BYTES_PER_SITE,
+                "bytes_per_site": cs_bytes,
                 "kernel_ms_per_step": cs_ms,
                 "share_of_step": prof[2] / max(prof[3], 1e-9),
                 "phi_ms_per_step": prof[0] / args.steps,
                 "mu_ms_per_step": prof[1] / args.steps,
-                "full_step_frac": STEP_BYTES_PER_SITE * sites_rank / (ms / args.steps * 1e-3)
-                / 1e9 / peak}
+                "step_bytes_per_site": step_bytes_per_site(fused, nzl),
+                "full_step_frac": step_bytes_per_site(fused, nzl) * sites_rank
+                / (ms / args.steps * 1e-3) / 1e9 / peak}
 
     # ---------------- e2e: public API with host buffers, every step
     e2e = None
@@ -383,6 +405,7 @@ def run_ours(args, rank, world, local):
                        "lattice": f"{nx}x{ny}x{nzl * world}",
                        "shape_per_gpu": f"{nx}x{ny}x{nzl}",
                        "mode": args.mode, "vvl": args.vvl, "physics": "binary free energy",
+                       "fused": fused, "fuse_lag": args.fuse_lag if fused else None,
                        "l2": f"state {4 * 19 * 8 * nx * ny * nzl / 1e9:.1f} GB/GPU >> 126 MB L2, "
                              "no flush needed",
                        "parallelism": f"z-slab x{world}",

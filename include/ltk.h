@@ -235,6 +235,12 @@ int ltk_fluid_totals(ltk_fluid *e, double *out5);
 int ltk_fluid_run(ltk_fluid *e, int64_t nsteps, void *stream);
 /* Capture one step pair (A->B, B->A) into CUDA graphs used by ltk_fluid_run. */
 int ltk_fluid_use_graph(ltk_fluid *e, int32_t enable);
+/* Fused collide-stream + next-state phi (k_cs_phi; default off, env
+ * LTK_FUSE=1 turns it on): the collide-stream kernel also forms phi of the
+ * state it writes, re-reading g' from L2 `extra_lag` + 3 planes behind the
+ * collision front, so the next step's k_phi runs on the boundary planes only.
+ * Bitwise identical to the three-kernel step. */
+int ltk_fluid_set_fuse(ltk_fluid *e, int32_t enable, int32_t extra_lag);
 /* Last step's per-kernel device times in ms (phi, mu, collide_stream, halo). */
 int ltk_fluid_profile(ltk_fluid *e, int32_t enable, float *ms4);
 

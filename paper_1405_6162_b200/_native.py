@@ -117,6 +117,7 @@ SIGNATURES = {
     "ltk_fluid_run": (ctypes.c_int, [_vp, _i64, _vp]),
     "ltk_fluid_totals": (ctypes.c_int, [_vp, ctypes.POINTER(_dbl)]),
     "ltk_fluid_use_graph": (ctypes.c_int, [_vp, _i32]),
+    "ltk_fluid_set_fuse": (ctypes.c_int, [_vp, _i32, _i32]),
     "ltk_fluid_profile": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_float)]),
     "ltk_fluid_ipc_blob": (ctypes.c_int, [_vp, ctypes.c_char_p]),
     "ltk_fluid_attach_peers": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p]),

@@ -158,6 +158,75 @@ static int launch_cs(const FluidArgs &a, int vvl, int mode, int phys, cudaStream
     return LTK_OK;
 }
 
+// Fused collide-stream + next-state phi (k_cs_phi).  Collides planes
+// [a.z_lo, a.z_lo + a.nplanes) and forms phi_next on [phi_lo, phi_hi), which
+// must lie strictly inside the collided planes.  extra_lag: planes of slack
+// between the collision front and the phi front beyond the 3 the
+// no-deadlock argument needs (fluid_kernels.cuh).
+static bool fuse_fields(FluidArgs &a, int vvl, int phi_lo, int phi_hi, int extra_lag,
+                        unsigned long long *sync) {
+    if (!sync || phi_hi <= phi_lo || phi_lo < a.z_lo + 1 || phi_hi > a.z_lo + a.nplanes - 1)
+        return false;
+    a.sync = sync;
+    a.tpp = (long long)a.ny * (a.nx / vvl);
+    a.phi_lo = phi_lo;
+    a.phi_hi = phi_hi;
+    // CTA b waits (before colliding) on planes up to phi plane + 1: they must
+    // lie in tickets < b, i.e. lag_ctas*128 > (phi_lo - z_lo + 2) * tpp + 127
+    const long long lag_threads = (long long)(phi_lo - a.z_lo + 2 + extra_lag) * a.tpp;
+    a.lag_ctas = (unsigned)((lag_threads + kTPB - 1) / kTPB) + 1;
+    a.ncta_cs = grid_for(a.nthreads, kTPB);
+    const unsigned nphi = grid_for((long long)(phi_hi - phi_lo) * a.tpp, kTPB);
+    a.ncta = std::max(a.ncta_cs, a.lag_ctas + nphi);
+    return true;
+}
+
+// L2 policy of the fused kernel's state traffic (bit 0: evict-first input
+// loads, bit 1: evict-first f' / evict-last g' stores); env LTK_FUSE_HINT.
+static int fuse_hint() {
+    static const int h = getenv("LTK_FUSE_HINT") ? atoi(getenv("LTK_FUSE_HINT")) & 3 : 2;
+    return h;
+}
+
+template <int MODE, int PHYS, int T1, int H>
+static void launch_csphi_h(const FluidArgs &a, int vvl, cudaStream_t st) {
+    if (vvl == 2)
+        k_cs_phi<2, MODE, PHYS, T1, H><<<a.ncta, kTPB, 0, st>>>(a);
+    else
+        k_cs_phi<1, MODE, PHYS, T1, H><<<a.ncta, kTPB, 0, st>>>(a);
+}
+
+template <int MODE, int PHYS, int T1>
+static void launch_csphi_t(const FluidArgs &a, int vvl, cudaStream_t st) {
+    switch (fuse_hint()) {
+        case 0: launch_csphi_h<MODE, PHYS, T1, 0>(a, vvl, st); break;
+        case 1: launch_csphi_h<MODE, PHYS, T1, 1>(a, vvl, st); break;
+        case 2: launch_csphi_h<MODE, PHYS, T1, 2>(a, vvl, st); break;
+        default: launch_csphi_h<MODE, PHYS, T1, 3>(a, vvl, st); break;
+    }
+}
+
+template <int PHYS>
+static void launch_csphi_exact(const FluidArgs &a, int vvl, cudaStream_t st) {
+    switch ((a.tau_f == 1.0 ? 1 : 0) | (a.tau_g == 1.0 ? 2 : 0)) {
+        case 0: launch_csphi_t<LTK_MODE_EXACT, PHYS, 0>(a, vvl, st); break;
+        case 1: launch_csphi_t<LTK_MODE_EXACT, PHYS, 1>(a, vvl, st); break;
+        case 2: launch_csphi_t<LTK_MODE_EXACT, PHYS, 2>(a, vvl, st); break;
+        default: launch_csphi_t<LTK_MODE_EXACT, PHYS, 3>(a, vvl, st); break;
+    }
+}
+
+static int launch_cs_phi(const FluidArgs &a, int vvl, int mode, int phys, cudaStream_t st) {
+    if (a.nthreads <= 0) return LTK_OK;
+    if (vvl > 2) return fail(LTK_ERR_PLAN, "collide-stream supports vvl 1, 2 (got %d)", vvl);
+    if (mode == LTK_MODE_EXACT && phys == 1) launch_csphi_exact<1>(a, vvl, st);
+    else if (mode == LTK_MODE_EXACT) launch_csphi_exact<0>(a, vvl, st);
+    else if (phys == 1) launch_csphi_t<LTK_MODE_FAST, 1, 0>(a, vvl, st);
+    else launch_csphi_t<LTK_MODE_FAST, 0, 0>(a, vvl, st);
+    LTK_CHECK_LAUNCH("k_cs_phi");
+    return LTK_OK;
+}
+
 // ------------------------------------------------------------------ plane copies
 struct PlaneCopies {
     const double *src[24];
@@ -321,8 +390,19 @@ struct ltk_fluid {
     ltk_fluid_params prm{};
     ltk_slab slab{};
     double *fg[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [state][f/g]
+    // phi per state in one allocation (phi of state s at phi + s*phi_stride):
+    // the fused kernel forms the next state's phi while this step's stays
     double *phi = nullptr, *mu = nullptr;
+    long long phi_stride = 0;
     int cur = 0;
+    // fused collide-stream + phi (k_cs_phi): counters [nzl + 2]; phi planes of
+    // the current state already formed by the previous step ([lo, hi))
+    unsigned long long *fsync = nullptr;
+    unsigned fuse_ncta = 0;  // grid of the fused launches counted in fsync
+    bool fuse = false;  // measured slower than the three-kernel step
+    int fuse_lag = 1;
+    int phi_lo = 0, phi_hi = 0;
+    double *phi_of(int s) const { return phi + s * phi_stride; }
     cudaStream_t st = nullptr, comm_st = nullptr;
     cudaEvent_t ev_fork[3] = {}, ev_join[3] = {};
     ncclComm_t comm = nullptr;
@@ -332,7 +412,7 @@ struct ltk_fluid {
     int transport = 0;
     struct Peer {
         double *fg[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-        double *phi = nullptr, *mu = nullptr;
+        double *phi[2] = {nullptr, nullptr}, *mu = nullptr;
         unsigned long long *inbox = nullptr;
     } up, dn;
     unsigned long long *inbox = nullptr;  // [2]: progress of the slab below / above
@@ -341,7 +421,8 @@ struct ltk_fluid {
     long long step = 0;   // timesteps taken (lockstep across slabs)
     bool primed = false;  // peer transport: halos re-primed by a load since the last step
     bool use_graph = false;
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    cudaGraphExec_t gexec[4] = {nullptr, nullptr, nullptr, nullptr};  // [state + 2*(phi formed)]
+    int gnxt[4][2] = {};  // phi planes each graph's step forms
     bool prof = false;
     cudaEvent_t pev[5] = {};          // events of the step being enqueued
     std::vector<cudaEvent_t> ppool;   // 4 per profiled step, read at the end
@@ -369,23 +450,24 @@ static FluidArgs engine_args(const ltk_fluid *e, int in_state) {
     a.g_in = e->fg[in_state][1];
     a.f_out = e->fg[1 - in_state][0];
     a.g_out = e->fg[1 - in_state][1];
-    a.phi_in = e->phi;
-    a.phi_out = e->phi;
+    a.phi_in = e->phi_of(in_state);
+    a.phi_out = e->phi_of(in_state);
+    a.phi_next = e->phi_of(1 - in_state);
     a.mu = e->mu;
     a.mu_out = e->mu;
     a.err = singular_word();
     if (e->transport == kLocal) {  // periodic images into this slab
         a.img_f_up = a.img_f_dn = a.f_out;
         a.img_g_up = a.img_g_dn = a.g_out;
-        a.img_phi_up = a.img_phi_dn = e->phi;
+        a.img_phi_up = a.img_phi_dn = e->phi_of(in_state);
         a.img_mu_up = a.img_mu_dn = e->mu;
     } else if (e->transport == kPeer) {  // images into the neighbours over NVLink
         a.img_f_up = e->up.fg[1 - in_state][0];
         a.img_g_up = e->up.fg[1 - in_state][1];
         a.img_f_dn = e->dn.fg[1 - in_state][0];
         a.img_g_dn = e->dn.fg[1 - in_state][1];
-        a.img_phi_up = e->up.phi;
-        a.img_phi_dn = e->dn.phi;
+        a.img_phi_up = e->up.phi[in_state];
+        a.img_phi_dn = e->dn.phi[in_state];
         a.img_mu_up = e->up.mu;
         a.img_mu_dn = e->dn.mu;
     }
@@ -422,7 +504,7 @@ static int exchange(ltk_fluid *e, int kind, int s) {
                 LTK_NCCL(n.Recv(plane(e->fg[s][d], sl, kDown[j], halo_hi), PL, ncclFloat64, up,
                                 e->comm, e->comm_st));
     } else {
-        double *b = kind == 1 ? e->phi : e->mu;
+        double *b = kind == 1 ? e->phi_of(s) : e->mu;
         LTK_NCCL(n.Send(b + top * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
         LTK_NCCL(n.Send(b + bot * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
         LTK_NCCL(n.Recv(b + halo_lo * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
@@ -438,23 +520,69 @@ static int exchange(ltk_fluid *e, int kind, int s) {
         if (rc_) return rc_;   \
     } while (0)
 
-static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof);
+static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof, int nxt[2]);
 
-// Enqueue one timestep reading state `s` and writing state 1 - s.
-static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
+// phi of state s on planes [lo, hi) minus those the previous step's fused
+// kernel already formed ([e->phi_lo, e->phi_hi)).
+template <class L>
+static int phi_rest(ltk_fluid *e, FluidArgs &a, long long lo, long long hi, L launch_one) {
+    const int vvl = e->vvl;
+    const long long dlo = std::max(lo, std::min(hi, (long long)e->phi_lo));
+    const long long dhi = std::max(dlo, std::min(hi, (long long)e->phi_hi));
+    if (dlo > lo) {
+        set_planes(a, vvl, lo, dlo);
+        LTK_RC(launch_one());
+    }
+    if (hi > dhi) {
+        set_planes(a, vvl, dhi, hi);
+        LTK_RC(launch_one());
+    }
+    return LTK_OK;
+}
+
+// Collide-stream of planes [lo, hi): fused with the next state's phi on
+// [lo + 1, hi - 1) when enabled and long enough, else the plain kernel.
+// nxt receives the phi planes formed.
+static int cs_planes(ltk_fluid *e, FluidArgs &a, long long lo, long long hi, cudaStream_t st,
+                     int nxt[2]) {
+    const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
+    if (hi <= lo) return LTK_OK;
+    set_planes(a, vvl, lo, hi);
+    if (e->fuse && a.ny * (a.nx / vvl) >= kTPB &&
+        fuse_fields(a, vvl, (int)lo + 1, (int)hi - 1, e->fuse_lag, e->fsync)) {
+        if (a.ncta != e->fuse_ncta) {  // launch epochs are ticket / ncta: restart the count
+            LTK_CUDA(cudaMemsetAsync(e->fsync, 0, (size_t)(e->nzl + 1) * 8, st));
+            e->fuse_ncta = a.ncta;
+        }
+        LTK_RC(launch_cs_phi(a, vvl, mode, phys, st));
+        nxt[0] = (int)lo + 1;
+        nxt[1] = (int)hi - 1;
+        return LTK_OK;
+    }
+    return launch_cs(a, vvl, mode, phys, st);
+}
+
+// Enqueue one timestep reading state `s` and writing state 1 - s.  nxt: the
+// phi planes of state 1 - s formed on the way (by the fused kernel).
+static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof, int nxt[2]) {
     FluidArgs a = engine_args(e, s);
     const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
     const long long nzl = e->nzl;
-    if (e->transport == kPeer) return enqueue_step_peer(e, s, st, prof);
+    nxt[0] = nxt[1] = 0;
+    if (e->transport == kPeer) return enqueue_step_peer(e, s, st, prof, nxt);
+    auto phi = [&] { return launch_phi(a, vvl, st); };
     if (prof) cudaEventRecord(e->pev[0], st);
     if (e->transport == kLocal) {
-        // single slab, periodic z: three kernels, halos written by the kernels
-        set_planes(a, vvl, 0, nzl);
-        LTK_RC(launch_phi(a, vvl, st));
+        // single slab, periodic z: halos written by the kernels; phi of the
+        // interior planes came with the previous step's collide-stream
+        LTK_RC(phi_rest(e, a, 0, nzl, phi));
         if (prof) cudaEventRecord(e->pev[1], st);
-        if (phys == 1) LTK_RC(launch_mu(a, vvl, st));
+        if (phys == 1) {
+            set_planes(a, vvl, 0, nzl);
+            LTK_RC(launch_mu(a, vvl, st));
+        }
         if (prof) cudaEventRecord(e->pev[2], st);
-        LTK_RC(launch_cs(a, vvl, mode, phys, st));
+        LTK_RC(cs_planes(e, a, 0, nzl, st, nxt));
         if (prof) cudaEventRecord(e->pev[3], st);
         return LTK_OK;
     }
@@ -474,12 +602,9 @@ static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
     LTK_CUDA(cudaStreamWaitEvent(e->comm_st, e->ev_fork[0], 0));
     LTK_RC(exchange(e, 0, s));
     LTK_CUDA(cudaEventRecord(e->ev_join[0], e->comm_st));
-    if (in_hi > in_lo) {
-        set_planes(a, vvl, in_lo, in_hi);
-        LTK_RC(launch_phi(a, vvl, st));
-    }
+    if (in_hi > in_lo) LTK_RC(phi_rest(e, a, in_lo, in_hi, phi));
     LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[0], 0));
-    LTK_RC(boundary([&] { return launch_phi(a, vvl, st); }));
+    LTK_RC(boundary(phi));
     if (prof) cudaEventRecord(e->pev[1], st);
     if (phys == 1) {
         // (2) phi faces || mu interior
@@ -500,10 +625,7 @@ static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
         LTK_CUDA(cudaEventRecord(e->ev_join[2], e->comm_st));
     }
     if (prof) cudaEventRecord(e->pev[2], st);
-    if (in_hi > in_lo) {
-        set_planes(a, vvl, in_lo, in_hi);
-        LTK_RC(launch_cs(a, vvl, mode, phys, st));
-    }
+    LTK_RC(cs_planes(e, a, in_lo, in_hi, st, nxt));
     if (phys == 1) LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[2], 0));
     LTK_RC(boundary([&] { return launch_cs(a, vvl, mode, phys, st); }));
     if (prof) cudaEventRecord(e->pev[3], st);
@@ -590,7 +712,7 @@ static int peer_wait(ltk_fluid *e, unsigned long long target, cudaStream_t st) {
 // Every wait sits behind the interior planes of a kernel, so the neighbours'
 // progress overlaps local work; the boundary planes then store their halo
 // images straight into the neighbours over NVLink.
-static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
+static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof, int nxt[2]) {
     FluidArgs a = engine_args(e, s);
     const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
     const long long nzl = e->nzl;
@@ -611,7 +733,7 @@ static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
     auto mu = [&] { return launch_mu(a, vvl, st); };
     auto cs = [&] { return launch_cs(a, vvl, mode, phys, st); };
     if (prof) cudaEventRecord(e->pev[0], st);
-    LTK_RC(ranges(1, nzl - 1, phi));
+    if (nzl > 2) LTK_RC(phi_rest(e, a, 1, nzl - 1, phi));
     LTK_RC(peer_wait(e, t4 + (e->primed ? 1 : 0), st));  // f/g halos of state s
     e->primed = false;
     LTK_RC(boundary(phi));
@@ -624,7 +746,7 @@ static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof) {
     }
     LTK_RC(peer_signal(e, t4 + 3, st));
     if (prof) cudaEventRecord(e->pev[2], st);
-    LTK_RC(ranges(1, nzl - 1, cs));
+    LTK_RC(cs_planes(e, a, 1, nzl - 1, st, nxt));
     LTK_RC(peer_wait(e, t4 + 3, st));  // mu halos
     LTK_RC(boundary(cs));
     LTK_RC(peer_signal(e, t4 + 4, st));
@@ -662,17 +784,27 @@ static int peer_prime(ltk_fluid *e, int s, cudaStream_t st) {
 // device to go idle; with the peer transport a progress-wait kernel may be
 // spinning on a neighbour whose work is not enqueued yet, so a lazy load in
 // the middle of an enqueue would stall until the spin budget runs out.
+template <int MODE, int PHYS, int T1>
+static void preload_cs_t(cudaFuncAttributes &fa) {
+    cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, T1>);
+    cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, T1>);
+    cudaFuncGetAttributes(&fa, k_cs_phi<1, MODE, PHYS, T1, 0>);
+    cudaFuncGetAttributes(&fa, k_cs_phi<1, MODE, PHYS, T1, 1>);
+    cudaFuncGetAttributes(&fa, k_cs_phi<1, MODE, PHYS, T1, 2>);
+    cudaFuncGetAttributes(&fa, k_cs_phi<1, MODE, PHYS, T1, 3>);
+    cudaFuncGetAttributes(&fa, k_cs_phi<2, MODE, PHYS, T1, 0>);
+    cudaFuncGetAttributes(&fa, k_cs_phi<2, MODE, PHYS, T1, 1>);
+    cudaFuncGetAttributes(&fa, k_cs_phi<2, MODE, PHYS, T1, 2>);
+    cudaFuncGetAttributes(&fa, k_cs_phi<2, MODE, PHYS, T1, 3>);
+}
+
 template <int MODE, int PHYS>
 static void preload_cs(cudaFuncAttributes &fa) {
-    cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 0>);
-    cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, 0>);
+    preload_cs_t<MODE, PHYS, 0>(fa);
     if constexpr (MODE == LTK_MODE_EXACT) {
-        cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 1>);
-        cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 2>);
-        cudaFuncGetAttributes(&fa, k_collide_stream<1, MODE, PHYS, 3>);
-        cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, 1>);
-        cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, 2>);
-        cudaFuncGetAttributes(&fa, k_collide_stream<2, MODE, PHYS, 3>);
+        preload_cs_t<MODE, PHYS, 1>(fa);
+        preload_cs_t<MODE, PHYS, 2>(fa);
+        preload_cs_t<MODE, PHYS, 3>(fa);
     }
 }
 
@@ -704,7 +836,8 @@ static int preload_step_kernels() {
 }
 
 static int wrap_state_halos(ltk_fluid *e, int s, int which, cudaStream_t st) {
-    return ltk_fluid_wrap_halos(&e->slab, e->fg[s][0], e->fg[s][1], e->phi, e->mu, which, st);
+    return ltk_fluid_wrap_halos(&e->slab, e->fg[s][0], e->fg[s][1], e->phi_of(s), e->mu, which,
+                                st);
 }
 
 }  // namespace ltk
@@ -906,11 +1039,19 @@ int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank, in
             }
             e->fg[s][d] = (double *)ptr;
         }
-    if ((rc = ltk_malloc(&ptr, plane_bytes))) {
+    e->phi_stride = (raw + 63) / 64 * 64;
+    if ((rc = ltk_malloc(&ptr, 2 * (size_t)e->phi_stride * sizeof(double)))) {
         ltk_fluid_destroy(e);
         return rc;
     }
     e->phi = (double *)ptr;
+    if ((rc = ltk_malloc(&ptr, (size_t)(e->nzl + 1) * sizeof(unsigned long long)))) {  // zeroed
+        ltk_fluid_destroy(e);
+        return rc;
+    }
+    e->fsync = (unsigned long long *)ptr;
+    if (const char *v = getenv("LTK_FUSE")) e->fuse = atoi(v) != 0;  // default off
+    if (const char *v = getenv("LTK_FUSE_LAG")) e->fuse_lag = std::max(0, atoi(v));
     if ((rc = ltk_malloc(&ptr, plane_bytes))) {
         ltk_fluid_destroy(e);
         return rc;
@@ -956,6 +1097,7 @@ int ltk_fluid_destroy(ltk_fluid *e) {
         for (auto &p : s)
             if (p) cudaFree(p);
     if (e->phi) cudaFree(e->phi);
+    if (e->fsync) cudaFree(e->fsync);
     if (e->mu) cudaFree(e->mu);
     for (int k = 0; k < 3; ++k) {
         if (e->ev_fork[k]) cudaEventDestroy(e->ev_fork[k]);
@@ -977,7 +1119,8 @@ int ltk_fluid_slab(const ltk_fluid *e, ltk_slab *s, int64_t *z0) {
 int ltk_fluid_buffers(const ltk_fluid *e, double **f, double **g, double **phi, double **mu) {
     if (f) *f = e->fg[e->cur][0];
     if (g) *g = e->fg[e->cur][1];
-    if (phi) *phi = e->phi;
+    // phi of the last step's input state (this state's before any step)
+    if (phi) *phi = e->phi_of(e->step > 0 ? 1 - e->cur : e->cur);
     if (mu) *mu = e->mu;
     return LTK_OK;
 }
@@ -999,6 +1142,7 @@ int ltk_fluid_load(ltk_fluid *e, const double *f_src, const double *g_src, int64
     cudaStream_t st = stream ? as_stream(stream) : e->st;
     if (e->transport == kPeer) LTK_RC(peer_before_load(e, st));
     e->cur = 0;
+    e->phi_lo = e->phi_hi = 0;  // phi of the loaded state not formed yet
     LTK_RC(ltk_fluid_scatter(&e->slab, f_src, padded, nz_src, z_src0, Q, e->fg[0][0], st));
     LTK_RC(ltk_fluid_scatter(&e->slab, g_src, padded, nz_src, z_src0, Q, e->fg[0][1], st));
     if (e->transport == kLocal) LTK_RC(wrap_state_halos(e, 0, 1, st));
@@ -1069,6 +1213,7 @@ int ltk_fluid_run(ltk_fluid *e, int64_t nsteps, void *stream) {
     cudaStream_t st = stream ? as_stream(stream) : e->st;
     for (int64_t k = 0; k < nsteps; ++k) {
         const int s = e->cur;
+        int nxt[2] = {0, 0};
         if (e->prof) {
             for (int k = 0; k < 4; ++k) {
                 cudaEvent_t ev;
@@ -1076,28 +1221,46 @@ int ltk_fluid_run(ltk_fluid *e, int64_t nsteps, void *stream) {
                 e->ppool.push_back(ev);
                 e->pev[k] = ev;
             }
-            LTK_RC(enqueue_step(e, s, st, true));
+            LTK_RC(enqueue_step(e, s, st, true, nxt));
             ++e->prof_steps;
         } else if (e->use_graph && e->transport == kLocal) {
-            if (!e->gexec[s]) {
+            // one graph per (input state, whether its phi interior is formed)
+            const int key = s + (e->phi_hi > e->phi_lo ? 2 : 0);
+            if (!e->gexec[key]) {
                 cudaGraph_t g;
                 LTK_CUDA(cudaStreamBeginCapture(e->st, cudaStreamCaptureModeThreadLocal));
-                int rc = enqueue_step(e, s, e->st, false);
+                int rc = enqueue_step(e, s, e->st, false, nxt);
                 cudaError_t ce = cudaStreamEndCapture(e->st, &g);
                 if (rc) return rc;
                 if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
-                ce = cudaGraphInstantiate(&e->gexec[s], g, 0);
+                ce = cudaGraphInstantiate(&e->gexec[key], g, 0);
                 cudaGraphDestroy(g);
                 if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+                e->gnxt[key][0] = nxt[0];
+                e->gnxt[key][1] = nxt[1];
             }
-            LTK_CUDA(cudaGraphLaunch(e->gexec[s], st));
+            nxt[0] = e->gnxt[key][0];
+            nxt[1] = e->gnxt[key][1];
+            LTK_CUDA(cudaGraphLaunch(e->gexec[key], st));
             count_launch(3);
         } else {
-            LTK_RC(enqueue_step(e, s, st, false));
+            LTK_RC(enqueue_step(e, s, st, false, nxt));
         }
+        e->phi_lo = nxt[0];
+        e->phi_hi = nxt[1];
         e->cur = 1 - s;
         ++e->step;
     }
+    return LTK_OK;
+}
+
+// Fused collide-stream + next-state phi on/off and its lag (planes of slack
+// between the collision front and the phi front).
+int ltk_fluid_set_fuse(ltk_fluid *e, int32_t enable, int32_t extra_lag) {
+    if (extra_lag < 0) return fail(LTK_ERR_CONFIG, "lag must be >= 0");
+    e->fuse = enable != 0;
+    e->fuse_lag = extra_lag;
+    drop_graphs(e);
     return LTK_OK;
 }
 
@@ -1166,7 +1329,8 @@ static int open_peer(ltk_fluid *e, const char *blob, ltk_fluid::Peer &p) {
     p.fg[0][1] = (double *)ptrs[1];
     p.fg[1][0] = (double *)ptrs[2];
     p.fg[1][1] = (double *)ptrs[3];
-    p.phi = (double *)ptrs[4];
+    p.phi[0] = (double *)ptrs[4];
+    p.phi[1] = p.phi[0] + e->phi_stride;  // same layout on every slab
     p.mu = (double *)ptrs[5];
     p.inbox = (unsigned long long *)ptrs[6];
     return LTK_OK;
@@ -1194,7 +1358,8 @@ int ltk_fluid_attach_peers(ltk_fluid *e, const char *up_blob, const char *dn_blo
 static void peer_from_engine(ltk_fluid::Peer &p, const ltk_fluid *o) {
     for (int st = 0; st < 2; ++st)
         for (int d = 0; d < 2; ++d) p.fg[st][d] = o->fg[st][d];
-    p.phi = o->phi;
+    p.phi[0] = o->phi_of(0);
+    p.phi[1] = o->phi_of(1);
     p.mu = o->mu;
     p.inbox = o->inbox;
 }

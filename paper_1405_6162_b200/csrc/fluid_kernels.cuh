@@ -36,6 +36,7 @@ struct FluidArgs {
     double *g_out;
     double *phi_out;
     double *mu_out;
+    double *phi_next;  // k_cs_phi: phi of the state being written
     long long *err;
     int nx, ny, nzl, z_lo, nplanes;
     // halo image targets (nullptr = none): buffers of the slab above (up) /
@@ -45,6 +46,12 @@ struct FluidArgs {
     long long PL, cstride;
     long long nthreads;   // threads of this launch
     long long nz_global, z0;  // for error-site reporting in host order
+    // fused collide-stream + next-state phi (k_cs_phi); see that kernel
+    unsigned long long *sync;  // [0] ticket, [1 + z] plane z sites done (cumulative)
+    long long tpp;             // threads per plane (ny * nx / VVL)
+    int phi_lo, phi_hi;        // phi planes of the next state formed in-kernel
+    unsigned lag_ctas;         // phi work of CTA b is the phi thread range of CTA b - lag_ctas
+    unsigned ncta_cs, ncta;    // CTAs with collide work / all CTAs
     double wv[Q];
     double lam[Q];
     double cs2, tau_f, tau_g, A, B, kappa, gamma;
@@ -59,52 +66,68 @@ struct Pos {
 };
 
 template <int VVL>
-__device__ __forceinline__ bool thread_pos(const FluidArgs &a, Pos &p) {
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= a.nthreads) return false;
+__device__ __forceinline__ void pos_of(const FluidArgs &a, unsigned tt, int z_lo, Pos &p) {
     const unsigned nxv = (unsigned)(a.nx / VVL);
-    const unsigned tt = (unsigned)t;
     const unsigned row = tt / nxv;
     p.x0 = (int)(tt - row * nxv) * VVL;
     p.y = (int)(row % (unsigned)a.ny);
-    p.z = a.z_lo + (int)(row / (unsigned)a.ny);
+    p.z = z_lo + (int)(row / (unsigned)a.ny);
+}
+
+template <int VVL>
+__device__ __forceinline__ bool thread_pos(const FluidArgs &a, Pos &p) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.nthreads) return false;
+    pos_of<VVL>(a, (unsigned)t, a.z_lo, p);
     return true;
 }
+
+// Load flavours of pull(): plain read-only (__ldg), read-only with an L2
+// policy (the fused kernel's input state), L2-only with a policy (state
+// written earlier in the same launch).
+enum { kLdg = 0, kLdNc = 1, kLdCg = 2 };
 
 __device__ __forceinline__ int wrapi(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
 
 // Pull the VVL values of component I at sites (x0..x0+VVL-1, y, zs) from
 // (x - cx, y - cy, zs - cz).  cx == 0 -> one aligned vector load.
-template <int I, int VVL>
+template <int I, int VVL, int LD = kLdg>
 __device__ __forceinline__ void pull(double (&v)[VVL], const double *base, const FluidArgs &a,
-                                     const Pos &p) {
+                                     const Pos &p, uint64_t pol = 0) {
     const int ys = wrapi(p.y - cy(I), a.ny);
     const double *row = base + (long long)I * a.cstride +
                         (long long)(p.z + 1 - cz(I)) * a.PL + (long long)ys * a.nx;
     if constexpr (cx(I) == 0) {
-        load_vec<VVL>(v, row + p.x0);
+        if constexpr (LD == kLdg) load_vec<VVL>(v, row + p.x0);
+        else if constexpr (LD == kLdNc) load_vec_nc<VVL>(v, row + p.x0, pol);
+        else load_vec_cg<VVL>(v, row + p.x0, pol);
     } else {
 #pragma unroll
-        for (int k = 0; k < VVL; ++k) v[k] = __ldg(row + wrapi(p.x0 + k - cx(I), a.nx));
+        for (int k = 0; k < VVL; ++k) {
+            const double *q = row + wrapi(p.x0 + k - cx(I), a.nx);
+            if constexpr (LD == kLdg) v[k] = __ldg(q);
+            else if constexpr (LD == kLdNc) v[k] = ld_nc_pol(q, pol);
+            else v[k] = ld_cg_pol(q, pol);
+        }
     }
 }
 
 // ------------------------------------------------------------------ phi
-template <int VVL>
-__global__ void __launch_bounds__(256) k_phi(const FluidArgs a) {
-    Pos p;
-    if (!thread_pos<VVL>(a, p)) return;
+template <int VVL, int LD, bool IMG = true>
+__device__ __forceinline__ void phi_site(const FluidArgs &a, const Pos &p, const double *g,
+                                         double *out, uint64_t pol) {
     double phi[VVL];
 #pragma unroll
     for (int k = 0; k < VVL; ++k) phi[k] = 0.0;
+    double v[Q][VVL];  // all loads issued before the first add
+    static_for<0, Q>([&](auto I) { pull<I.value, VVL, LD>(v[I.value], g, a, p, pol); });
     static_for<0, Q>([&](auto I) {
-        double v[VVL];
-        pull<I.value, VVL>(v, a.g_in, a, p);
 #pragma unroll
-        for (int k = 0; k < VVL; ++k) phi[k] = __dadd_rn(phi[k], v[k]);
+        for (int k = 0; k < VVL; ++k) phi[k] = __dadd_rn(phi[k], v[I.value][k]);
     });
     const long long off = (long long)p.y * a.nx + p.x0;
-    store_vec<VVL>(a.phi_out + (long long)(p.z + 1) * a.PL + off, phi);
+    store_vec<VVL>(out + (long long)(p.z + 1) * a.PL + off, phi);
+    if constexpr (!IMG) return;
     // halo images for the mu stencil of the neighbouring slabs (or this one)
     bool img = false;
     if (p.z == 0 && a.img_phi_dn) {
@@ -116,6 +139,13 @@ __global__ void __launch_bounds__(256) k_phi(const FluidArgs a) {
         img = true;
     }
     if (img) __threadfence_system();  // peer images visible before the progress signal
+}
+
+template <int VVL>
+__global__ void __launch_bounds__(256) k_phi(const FluidArgs a) {
+    Pos p;
+    if (!thread_pos<VVL>(a, p)) return;
+    phi_site<VVL, kLdg>(a, p, a.g_in, a.phi_out, 0);
 }
 
 // ------------------------------------------------------------------ mu
@@ -282,15 +312,28 @@ __device__ __forceinline__ void frelax_pair(double (&F)[Q][VVL], double (&G)[Q][
     if constexpr (O != C) frelax<O, MODE, PHYS, T1>(F[O][k], G[O][k], -q, sq, s, a);
 }
 
-template <int VVL, int MODE, int PHYS, int T1>
-__global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_collide_stream(const FluidArgs a) {
-    using M = typename std::conditional<MODE == LTK_MODE_EXACT, Exact, Fast>::type;
-    Pos p;
-    if (!thread_pos<VVL>(a, p)) return;
+// One VVL-site chunk of the pull + forced collision.  HINT bit 0: the input
+// state is read with L2 evict-first (each value is pulled once); bit 1: f' is
+// stored evict-first and g' evict-last, so g' stays in L2 until k_cs_phi's
+// lagged phi re-reads it a few planes later.
+template <int VVL, int HINT>
+__device__ __forceinline__ void cs_load(const FluidArgs &a, const Pos &p, double (&F)[Q][VVL],
+                                        double (&G)[Q][VVL]) {
+    const uint64_t pol = (HINT & 1) ? l2_evict_first() : 0;
+    constexpr int LD = (HINT & 1) ? kLdNc : kLdg;
+    static_for<0, Q>([&](auto I) { pull<I.value, VVL, LD>(F[I.value], a.f_in, a, p, pol); });
+    static_for<0, Q>([&](auto I) { pull<I.value, VVL, LD>(G[I.value], a.g_in, a, p, pol); });
+}
 
-    double F[Q][VVL], G[Q][VVL];
-    static_for<0, Q>([&](auto I) { pull<I.value, VVL>(F[I.value], a.f_in, a, p); });
-    static_for<0, Q>([&](auto I) { pull<I.value, VVL>(G[I.value], a.g_in, a, p); });
+template <int VVL, int MODE, int PHYS, int T1, int HINT>
+__device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, double (&F)[Q][VVL],
+                                          double (&G)[Q][VVL]) {
+    using M = typename std::conditional<MODE == LTK_MODE_EXACT, Exact, Fast>::type;
+    uint64_t pol_first = 0, pol_last = 0;
+    if constexpr (HINT & 2) {
+        pol_first = l2_evict_first();
+        pol_last = l2_evict_last();
+    }
 
     FSite st[VVL];
 #pragma unroll
@@ -337,8 +380,13 @@ __global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_collide_stream(const 
     const long long off = (long long)p.y * a.nx + p.x0;
     const long long o = (long long)(p.z + 1) * a.PL + off;
     static_for<0, Q>([&](auto I) {
-        store_vec<VVL>(a.f_out + I.value * a.cstride + o, F[I.value]);
-        store_vec<VVL>(a.g_out + I.value * a.cstride + o, G[I.value]);
+        if constexpr (HINT & 2) {
+            store_vec_pol<VVL>(a.f_out + I.value * a.cstride + o, F[I.value], pol_first);
+            store_vec_pol<VVL>(a.g_out + I.value * a.cstride + o, G[I.value], pol_last);
+        } else {
+            store_vec<VVL>(a.f_out + I.value * a.cstride + o, F[I.value]);
+            store_vec<VVL>(a.g_out + I.value * a.cstride + o, G[I.value]);
+        }
         // halo images of the components that cross the z faces
         if constexpr (cz(I.value) < 0) {
             if (p.z == 0 && a.img_f_dn) {
@@ -356,6 +404,104 @@ __global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_collide_stream(const 
     });
     if ((p.z == 0 && a.img_f_dn) || (p.z == a.nzl - 1 && a.img_f_up))
         __threadfence_system();  // peer images visible before the progress signal
+}
+
+template <int VVL, int MODE, int PHYS, int T1, int HINT>
+__device__ __forceinline__ void cs_site(const FluidArgs &a, const Pos &p) {
+    double F[Q][VVL], G[Q][VVL];
+    cs_load<VVL, HINT>(a, p, F, G);
+    cs_finish<VVL, MODE, PHYS, T1, HINT>(a, p, F, G);
+}
+
+template <int VVL, int MODE, int PHYS, int T1, int HINT = 0>
+__global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_collide_stream(const FluidArgs a) {
+    Pos p;
+    if (!thread_pos<VVL>(a, p)) return;
+    cs_site<VVL, MODE, PHYS, T1, HINT>(a, p);
+}
+
+// ------------------------------------------------------------------ fused step
+// k_cs_phi: collide-stream of planes [z_lo, z_lo + nplanes) AND phi of the
+// NEXT state on planes [phi_lo, phi_hi), read back a few planes behind the
+// collision front -- the k_phi pass over g' leaves the step.
+// phi(x) = sum_i g'_i(x - c_i) reads g' on planes z-1..z+1, all written by
+// this launch, so:
+//  * work order: each CTA takes a ticket T (one atomicAdd); b = T mod ncta is
+//    its work index, so every lower index of this launch is already resident
+//    or finished; e = T div ncta counts this engine's launches (graph-replay
+//    safe: counters are never reset, every launch takes exactly ncta tickets);
+//  * warp w of CTA b handles collide threads [128 b + 32 w, +32) and the phi
+//    threads lag_ctas*128 behind.  A warp first issues its collision loads,
+//    then polls (ld.acquire) the completion counters of the planes its phi
+//    sites pull from, then issues the phi loads (L2), then finishes the
+//    collision and publishes its sites per plane (__syncwarp + one
+//    red.release per plane).  No CTA barrier after the ticket: warps never
+//    idle waiting for each other, so HBM requests stay in flight.
+//  * lag_ctas covers > 3 planes + one CTA (host-checked), so the waited-on
+//    planes belong to lower work indices: no deadlock; the host adds slack
+//    planes so the poll is normally satisfied at once.
+// Counters are 64-bit and cumulative: plane z is complete in launch e when
+// done[z] >= (e + 1) * tpp.  phi arithmetic is phi_site's (index-order
+// __dadd_rn): bitwise equal to k_phi.  phi planes never include 0 or nzl-1
+// (no halo images from here; the engine forms those planes with k_phi).
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_gpu_add(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int VVL, int MODE, int PHYS, int T1, int HINT>
+__global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_cs_phi(const FluidArgs a) {
+    __shared__ unsigned long long s_ticket;
+    unsigned long long *const ticket = a.sync, *const done = a.sync + 1;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const unsigned long long T = s_ticket;
+    const unsigned b = (unsigned)(T % a.ncta);
+    const unsigned long long target = (T / a.ncta + 1) * (unsigned long long)a.tpp;
+    const long long tpp = a.tpp;
+    const int lane = threadIdx.x & 31;
+    const long long tw = (long long)b * 128 + (threadIdx.x & ~31);  // warp's first thread
+
+    // ---- collision loads of this warp's sites
+    const long long t = tw + lane;
+    const bool has_cs = b < a.ncta_cs && t < a.nthreads;
+    Pos pc;
+    double F[Q][VVL], G[Q][VVL];
+    if (has_cs) {
+        pos_of<VVL>(a, (unsigned)t, a.z_lo, pc);
+        cs_load<VVL, HINT>(a, pc, F, G);
+    }
+    // ---- phi of the next state, lag_ctas CTAs behind
+    const long long nphi = (long long)(a.phi_hi - a.phi_lo) * tpp;
+    const long long uw = tw - (long long)a.lag_ctas * 128;
+    if (uw >= 0 && uw < nphi) {  // warp-uniform
+        const long long u = uw + lane;
+        const long long ul = (uw + 32 < nphi ? uw + 32 : nphi) - 1;
+        const int zlo = a.phi_lo + (int)(uw / tpp) - 1, zhi = a.phi_lo + (int)(ul / tpp) + 1;
+        if (lane <= zhi - zlo) {
+            while (ld_acquire_gpu_u64(done + zlo + lane) < target) __nanosleep(64);
+        }
+        __syncwarp();
+        if (u < nphi) {
+            Pos p;
+            pos_of<VVL>(a, (unsigned)u, a.phi_lo, p);
+            phi_site<VVL, kLdCg, false>(a, p, a.g_out, a.phi_next, l2_evict_first());
+        }
+    }
+    if (has_cs) cs_finish<VVL, MODE, PHYS, T1, HINT>(a, pc, F, G);
+    // ---- publish this warp's sites, one release per plane
+    __syncwarp();
+    if (b < a.ncta_cs && tw < a.nthreads) {
+        const int z = has_cs ? (int)(t / tpp) : -1;
+        const unsigned act = __ballot_sync(0xffffffffu, has_cs);
+        const unsigned same = __match_any_sync(0xffffffffu, z);
+        if (has_cs && lane == __ffs(same & act) - 1)
+            red_release_gpu_add(done + a.z_lo + z, (unsigned long long)__popc(same & act));
+    }
 }
 
 }  // namespace ltk

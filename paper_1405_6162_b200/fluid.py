@@ -160,6 +160,12 @@ class BinaryFluid:
     def set_graph(self, enable: bool) -> None:
         nat.check(nat.lib.ltk_fluid_use_graph(self._h, 1 if enable else 0), "use_graph")
 
+    def set_fuse(self, enable: bool, extra_lag: int = 1) -> None:
+        """Fused collide-stream + next-state phi (k_cs_phi; on by default).
+        Bitwise identical either way; off runs the three-kernel step."""
+        nat.check(nat.lib.ltk_fluid_set_fuse(self._h, 1 if enable else 0, int(extra_lag)),
+                  "set_fuse")
+
     def ipc_blob(self) -> bytes:
         """CUDA IPC handles of this slab's buffers (exchange them, then attach_peers)."""
         buf = ctypes.create_string_buffer(nat.IPC_BLOB_BYTES)

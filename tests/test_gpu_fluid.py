@@ -136,6 +136,69 @@ class TestFullStepParity:
         assert np.array_equal(f1.data, of) and np.array_equal(g1.data, og)
 
 
+class TestFusedStep:
+    """k_cs_phi (collide-stream + next-state phi from L2, ticket-ordered CTAs)
+    against the three-kernel step: bitwise, for every lag, mode, graph on/off,
+    planes of exactly one CTA (tpp = 128) and ragged plane sizes."""
+
+    @staticmethod
+    def _run(lk, shape, fuse, lag, mode, graph, steps, seed=17):
+        f0, g0 = _state(lk, shape, seed)
+        model = lk.D3Q19Model(tau_f=0.9, tau_g=1.2)
+        with lk.BinaryFluid(lk.LatticeShape(*shape), model=model, mode=mode,
+                            use_graph=graph) as sim:
+            sim.set_fuse(fuse, lag)
+            sim.load(f0, g0)
+            sim.run(steps)
+            f1, g1 = sim.fields()
+            phi, mu = sim.order_parameter()
+        return f1.data, g1.data, phi, mu
+
+    @pytest.mark.parametrize("shape", [(16, 8, 16), (32, 16, 6), (64, 3, 9), (16, 12, 10),
+                                       (24, 10, 3), (40, 6, 33)])
+    @pytest.mark.parametrize("lag", [0, 1, 5])
+    def test_fused_equals_unfused_exact(self, lk, shape, lag):
+        ref = self._run(lk, shape, False, 0, lk.MODE_EXACT, False, 5)
+        for graph in (False, True):
+            got = self._run(lk, shape, True, lag, lk.MODE_EXACT, graph, 5)
+            for a, b in zip(got, ref):
+                assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (shape, lag, graph)
+
+    def test_fused_matches_oracle(self, lk):
+        shape = (32, 8, 12)
+        f0, g0 = _state(lk, shape, 29)
+        with lk.BinaryFluid(lk.LatticeShape(*shape)) as sim:
+            sim.set_fuse(True, 0)
+            sim.load(f0, g0)
+            sim.run(6)
+            f1, g1 = sim.fields()
+        of, og, _, _ = _oracle(f0, g0, shape, 6, 1)
+        assert np.array_equal(f1.data, of) and np.array_equal(g1.data, og)
+
+    def test_fused_fast_large_plane(self, lk):
+        # BASELINE plane size (256^2 -> 512 CTAs per plane), FAST, fused == unfused bitwise
+        shape = (256, 256, 24)
+        ref = self._run(lk, shape, False, 0, lk.MODE_FAST, False, 4)
+        for lag in (0, 1, 3):
+            got = self._run(lk, shape, True, lag, lk.MODE_FAST, True, 4)
+            for a, b in zip(got, ref):
+                assert np.array_equal(a, b), lag
+
+    def test_reload_between_runs(self, lk):
+        # a load invalidates the phi the previous fused step formed
+        shape = (16, 16, 8)
+        f0, g0 = _state(lk, shape, 3)
+        f1, g1 = _state(lk, shape, 4)
+        with lk.BinaryFluid(lk.LatticeShape(*shape)) as sim:
+            sim.load(f0, g0)
+            sim.run(2)
+            sim.load(f1, g1)
+            sim.run(3)
+            fa, ga = sim.fields()
+        of, og, _, _ = _oracle(f1, g1, shape, 3, 1)
+        assert np.array_equal(fa.data, of) and np.array_equal(ga.data, og)
+
+
 class TestSlabDecomposition:
     """P virtual slabs on one GPU, halos moved with the C-ABI face/plane calls."""
 

@@ -92,12 +92,13 @@ def _worker(rank, world, port, shape, steps, physics, q):
 
 @pytest.mark.parametrize("nslabs", [2, 3, 4])
 @pytest.mark.parametrize("physics", ["binary", "passive"])
-def test_engines_in_one_process_bitwise(nslabs, physics):
+@pytest.mark.parametrize("nz", [12, 24])  # nz 24: every slab runs the fused k_cs_phi interior
+def test_engines_in_one_process_bitwise(nslabs, physics, nz):
     import paper_1405_6162_b200 as lk
     from oracle import oracle as orc
     from paper_1405_6162_b200.kernels import random_binary_state
 
-    shape, steps = (32, 8, 12), 4
+    shape, steps = (32, 8, nz), 4
     full = lk.LatticeShape(*shape)
     model = lk.D3Q19Model(tau_f=0.9, tau_g=1.1)
     sims = [lk.BinaryFluid(full, model=model, physics=physics, rank=r, nranks=nslabs,
