@@ -346,6 +346,9 @@ def run_ours(args, rank, world, local):
     ms = nat.elapsed_ms(start, stop)
     tot1 = [ctl.allreduce(float(v), "SUM") for v in sim.totals()]
     launches = nat.launch_count() - l_before
+    # peer transport: a progress wait that ran out of budget means stale halos
+    peer_timeout = bool(world > 1 and args.transport == "peer" and sim.peer_timed_out())
+    peer_timeout = ctl.allreduce(float(peer_timeout), "MAX") > 0
     ctl.barrier()
     clk = clocks.stop() if rank == 0 else None
     ms_max = ctl.allreduce(ms, "MAX")
@@ -412,6 +415,7 @@ def run_ours(args, rank, world, local):
                        "halo_transport": ("periodic images (one slab)" if world == 1 else
                                           args.transport)},
             "gpu_launches": launches_all,
+            "peer_wait_timeout": peer_timeout,
             "conservation": {"steps": args.warmup + args.steps,
                              "mass_rel_drift": abs(tot1[0] - tot0[0]) / abs(tot0[0]),
                              "phi_rel_drift": abs(tot1[4] - tot0[4]) / abs(tot0[4]),

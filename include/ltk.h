@@ -241,6 +241,14 @@ int ltk_fluid_use_graph(ltk_fluid *e, int32_t enable);
  * collision front, so the next step's k_phi runs on the boundary planes only.
  * Bitwise identical to the three-kernel step. */
 int ltk_fluid_set_fuse(ltk_fluid *e, int32_t enable, int32_t extra_lag);
+/* Collide-stream kernel variant, process-wide: LTK_CS_REG = register-resident
+ * loads (k_collide_stream), LTK_CS_TMA = state rows staged in shared memory by
+ * TMA bulk copies in a warp-specialised persistent kernel (k_cs_tma; nx a
+ * multiple of 128, VVL 1, else the register kernel).  Bitwise identical.
+ * variant < 0 only queries; *previous (if not NULL) gets the old value. */
+#define LTK_CS_REG 0
+#define LTK_CS_TMA 1
+int ltk_fluid_cs_variant(int32_t variant, int32_t *previous);
 /* Last step's per-kernel device times in ms (phi, mu, collide_stream, halo). */
 int ltk_fluid_profile(ltk_fluid *e, int32_t enable, float *ms4);
 

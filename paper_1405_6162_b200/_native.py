@@ -22,6 +22,8 @@ IPC_BLOB_BYTES = 512
 LTK_ERR_SINGULAR = 11
 MODE_EXACT = 0
 MODE_FAST = 1
+CS_REG = 0
+CS_TMA = 1
 
 _ERRORS = {1: ConfigError, 2: BoundsError, 3: ShapeError, 4: AllocationError,
            5: LifecycleError, 6: PlanError, 7: DeviceError, 11: SingularStateError}
@@ -118,6 +120,7 @@ SIGNATURES = {
     "ltk_fluid_totals": (ctypes.c_int, [_vp, ctypes.POINTER(_dbl)]),
     "ltk_fluid_use_graph": (ctypes.c_int, [_vp, _i32]),
     "ltk_fluid_set_fuse": (ctypes.c_int, [_vp, _i32, _i32]),
+    "ltk_fluid_cs_variant": (ctypes.c_int, [_i32, ctypes.POINTER(_i32)]),
     "ltk_fluid_profile": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_float)]),
     "ltk_fluid_ipc_blob": (ctypes.c_int, [_vp, ctypes.c_char_p]),
     "ltk_fluid_attach_peers": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p]),

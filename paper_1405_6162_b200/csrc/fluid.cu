@@ -16,7 +16,7 @@
 #include <new>
 #include <vector>
 
-#include "stencil_tma.cuh"
+#include "cs_tma.cuh"
 
 namespace ltk {
 
@@ -127,6 +127,18 @@ static int launch_mu(const FluidArgs &a, int vvl, cudaStream_t st) {
     return LTK_OK;
 }
 
+// collide-stream kernel variant (process-wide): LTK_CS_REG register-resident
+// k_collide_stream, LTK_CS_TMA TMA-staged k_cs_tma where it applies (nx a
+// multiple of 128, VVL 1).  Default from env LTK_CS_VARIANT, else TMA.
+static int &cs_variant() {
+    static int v = getenv("LTK_CS_VARIANT") ? atoi(getenv("LTK_CS_VARIANT")) : LTK_CS_REG;
+    return v;
+}
+
+static bool use_cs_tma(const FluidArgs &a, int vvl) {
+    return cs_variant() == LTK_CS_TMA && cs_tma_ok(a, vvl);
+}
+
 template <int MODE, int PHYS, int T1>
 static void launch_cs_t(const FluidArgs &a, int vvl, cudaStream_t st) {
     const unsigned g = grid_for(a.nthreads, kTPB);
@@ -135,6 +147,7 @@ static void launch_cs_t(const FluidArgs &a, int vvl, cudaStream_t st) {
     else
         k_collide_stream<1, MODE, PHYS, T1><<<g, kTPB, 0, st>>>(a);
 }
+
 
 template <int PHYS>
 static void launch_cs_exact(const FluidArgs &a, int vvl, cudaStream_t st) {
@@ -149,6 +162,7 @@ static void launch_cs_exact(const FluidArgs &a, int vvl, cudaStream_t st) {
 
 static int launch_cs(const FluidArgs &a, int vvl, int mode, int phys, cudaStream_t st) {
     if (a.nthreads <= 0) return LTK_OK;
+    if (use_cs_tma(a, vvl)) return launch_cs_tma(a, mode, phys, st);
     if (vvl > 2) return fail(LTK_ERR_PLAN, "collide-stream supports vvl 1, 2 (got %d)", vvl);
     if (mode == LTK_MODE_EXACT && phys == 1) launch_cs_exact<1>(a, vvl, st);
     else if (mode == LTK_MODE_EXACT) launch_cs_exact<0>(a, vvl, st);
@@ -1340,6 +1354,7 @@ int ltk_fluid_attach_peers(ltk_fluid *e, const char *up_blob, const char *dn_blo
     if (e->nranks < 2) return fail(LTK_ERR_CONFIG, "peer transport needs >= 2 slabs");
     if (e->transport != kLocal) return fail(LTK_ERR_CONFIG, "transport already attached");
     LTK_RC(preload_step_kernels());
+    preload_cs_tma((int)e->nx);
     LTK_RC(open_peer(e, up_blob, e->up));
     if (memcmp(up_blob, dn_blob, sizeof(IpcBlob)) == 0)
         e->dn = e->up;  // two slabs: both neighbours are the same rank
@@ -1370,6 +1385,7 @@ int ltk_fluid_attach_peer_engines(ltk_fluid *e, const ltk_fluid *up, const ltk_f
     if (up->slab.cstride != e->slab.cstride || dn->slab.cstride != e->slab.cstride)
         return fail(LTK_ERR_SHAPE, "peer slabs differ in layout");
     LTK_RC(preload_step_kernels());
+    preload_cs_tma((int)e->nx);
     peer_from_engine(e->up, up);
     peer_from_engine(e->dn, dn);
     // complete before returning: the legacy-stream memset must not land after
@@ -1387,6 +1403,16 @@ int ltk_fluid_peer_timeout(ltk_fluid *e, int32_t *timed_out) {
     int v = 0;
     LTK_CUDA(cudaMemcpy(&v, e->peer_timeout, sizeof v, cudaMemcpyDeviceToHost));
     *timed_out = v;
+    return LTK_OK;
+}
+
+int ltk_fluid_cs_variant(int32_t variant, int32_t *previous) {
+    if (previous) *previous = cs_variant();
+    if (variant >= 0) {
+        if (variant != LTK_CS_REG && variant != LTK_CS_TMA)
+            return fail(LTK_ERR_CONFIG, "unknown collide-stream variant %d", variant);
+        cs_variant() = variant;
+    }
     return LTK_OK;
 }
 

@@ -325,9 +325,30 @@ __device__ __forceinline__ void cs_load(const FluidArgs &a, const Pos &p, double
     static_for<0, Q>([&](auto I) { pull<I.value, VVL, LD>(G[I.value], a.g_in, a, p, pol); });
 }
 
-template <int VVL, int MODE, int PHYS, int T1, int HINT>
+// mu and its central gradient at lane k of the chunk, from the mu slab in
+// global memory: mu(x), ((mu(x+1) - mu(x-1)) * 0.5) per axis (oracle op order).
+template <int VVL>
+struct MuGlobal {
+    const FluidArgs &a;
+    const Pos &p;
+    __device__ __forceinline__ void operator()(int k, double &mu, double &gmx, double &gmy,
+                                               double &gmz) const {
+        const double *mc = a.mu + (long long)(p.z + 1) * a.PL;
+        const int yp = wrapi(p.y + 1, a.ny), ym = wrapi(p.y - 1, a.ny);
+        const int x = p.x0 + k;
+        const long long r = (long long)p.y * a.nx;
+        mu = __ldg(mc + r + x);
+        gmx = Exact::mul(Exact::sub(__ldg(mc + r + wrapi(x + 1, a.nx)),
+                                    __ldg(mc + r + wrapi(x - 1, a.nx))), 0.5);
+        gmy = Exact::mul(Exact::sub(__ldg(mc + (long long)yp * a.nx + x),
+                                    __ldg(mc + (long long)ym * a.nx + x)), 0.5);
+        gmz = Exact::mul(Exact::sub(__ldg(mc + a.PL + r + x), __ldg(mc - a.PL + r + x)), 0.5);
+    }
+};
+
+template <int VVL, int MODE, int PHYS, int T1, int HINT, class MuFn>
 __device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, double (&F)[Q][VVL],
-                                          double (&G)[Q][VVL]) {
+                                          double (&G)[Q][VVL], const MuFn &mufn) {
     using M = typename std::conditional<MODE == LTK_MODE_EXACT, Exact, Fast>::type;
     uint64_t pol_first = 0, pol_last = 0;
     if constexpr (HINT & 2) {
@@ -344,23 +365,12 @@ __device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, doub
         for (int k = 0; k < VVL; ++k) faccum<I.value, M>(st[k], F[I.value][k]);
     });
     bool ok[VVL];
-    const double *mc = a.mu + (long long)(p.z + 1) * a.PL;
-    const int yp = wrapi(p.y + 1, a.ny), ym = wrapi(p.y - 1, a.ny);
 #pragma unroll
     for (int k = 0; k < VVL; ++k) {
 #pragma unroll
         for (int i = 0; i < Q; ++i) st[k].phi = M::add(st[k].phi, G[i][k]);
         double gmx = 0.0, gmy = 0.0, gmz = 0.0;
-        if constexpr (PHYS == 1) {
-            const int x = p.x0 + k;
-            const long long r = (long long)p.y * a.nx;
-            st[k].mu = __ldg(mc + r + x);
-            gmx = Exact::mul(Exact::sub(__ldg(mc + r + wrapi(x + 1, a.nx)),
-                                        __ldg(mc + r + wrapi(x - 1, a.nx))), 0.5);
-            gmy = Exact::mul(Exact::sub(__ldg(mc + (long long)yp * a.nx + x),
-                                        __ldg(mc + (long long)ym * a.nx + x)), 0.5);
-            gmz = Exact::mul(Exact::sub(__ldg(mc + a.PL + r + x), __ldg(mc - a.PL + r + x)), 0.5);
-        }
+        if constexpr (PHYS == 1) mufn(k, st[k].mu, gmx, gmy, gmz);
         ok[k] = !(st[k].rho <= 0.0);
         if (ok[k]) {
             fsite_finish<MODE, PHYS>(st[k], gmx, gmy, gmz, a);
@@ -410,7 +420,7 @@ template <int VVL, int MODE, int PHYS, int T1, int HINT>
 __device__ __forceinline__ void cs_site(const FluidArgs &a, const Pos &p) {
     double F[Q][VVL], G[Q][VVL];
     cs_load<VVL, HINT>(a, p, F, G);
-    cs_finish<VVL, MODE, PHYS, T1, HINT>(a, p, F, G);
+    cs_finish<VVL, MODE, PHYS, T1, HINT>(a, p, F, G, MuGlobal<VVL>{a, p});
 }
 
 template <int VVL, int MODE, int PHYS, int T1, int HINT = 0>
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_cs_phi(const FluidArg
             phi_site<VVL, kLdCg, false>(a, p, a.g_out, a.phi_next, l2_evict_first());
         }
     }
-    if (has_cs) cs_finish<VVL, MODE, PHYS, T1, HINT>(a, pc, F, G);
+    if (has_cs) cs_finish<VVL, MODE, PHYS, T1, HINT>(a, pc, F, G, MuGlobal<VVL>{a, pc});
     // ---- publish this warp's sites, one release per plane
     __syncwarp();
     if (b < a.ncta_cs && tw < a.nthreads) {

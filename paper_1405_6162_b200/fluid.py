@@ -31,6 +31,8 @@ from .model import D3Q19Model, Q
 
 MODE_EXACT = nat.MODE_EXACT
 MODE_FAST = nat.MODE_FAST
+CS_REG = nat.CS_REG
+CS_TMA = nat.CS_TMA
 PHYSICS = {"passive": 0, "binary": 1}
 
 
@@ -304,6 +306,16 @@ class BinaryFluid:
         arr = (ctypes.c_float * 4)()
         nat.check(nat.lib.ltk_fluid_profile(self._h, 1 if enable else 0, arr), "profile")
         return [float(v) for v in arr]
+
+
+def cs_variant(variant: int | None = None) -> int:
+    """Collide-stream kernel used by every engine of the process: CS_REG
+    (register-resident loads) or CS_TMA (TMA-staged rows, warp-specialised).
+    Returns the previous value; None only queries."""
+    prev = ctypes.c_int32(0)
+    nat.check(nat.lib.ltk_fluid_cs_variant(-1 if variant is None else int(variant),
+                                           ctypes.byref(prev)), "cs_variant")
+    return int(prev.value)
 
 
 def nccl_unique_id() -> bytes:

@@ -199,6 +199,56 @@ class TestFusedStep:
         assert np.array_equal(fa.data, of) and np.array_equal(ga.data, og)
 
 
+class TestTmaCollideStream:
+    """k_cs_tma (state rows staged in shared memory by TMA bulk copies, warp-
+    specialised persistent CTAs) against the oracle and the register kernel:
+    bitwise in EXACT mode; row-edge wrap pieces for nx = 128, 256, 384."""
+
+    @staticmethod
+    def _run(lk, shape, variant, mode, steps, physics="binary", seed=41, graph=False):
+        f0, g0 = _state(lk, shape, seed)
+        model = lk.D3Q19Model(tau_f=0.85, tau_g=1.3)
+        prev = lk.cs_variant(variant)
+        try:
+            with lk.BinaryFluid(lk.LatticeShape(*shape), model=model, mode=mode, physics=physics,
+                                use_graph=graph) as sim:
+                sim.load(f0, g0)
+                sim.run(steps)
+                f1, g1 = sim.fields()
+        finally:
+            lk.cs_variant(prev)
+        return f0, g0, f1.data, g1.data
+
+    @pytest.mark.parametrize("shape", [(128, 4, 6), (256, 6, 5), (384, 2, 3), (128, 1, 4)])
+    @pytest.mark.parametrize("physics", ["binary", "passive"])
+    def test_tma_exact_matches_oracle(self, lk, shape, physics):
+        f0, g0, f1, g1 = self._run(lk, shape, lk.CS_TMA, lk.MODE_EXACT, 3, physics)
+        of, og, _, _ = _oracle(f0, g0, shape, 3, 1 if physics == "binary" else 0, 0.85, 1.3)
+        assert np.array_equal(f1.view(np.uint64), of.view(np.uint64))
+        assert np.array_equal(g1.view(np.uint64), og.view(np.uint64))
+
+    @pytest.mark.parametrize("graph", [False, True])
+    def test_tma_fast_equals_register_kernel(self, lk, graph):
+        shape = (256, 64, 16)
+        ref = self._run(lk, shape, lk.CS_REG, lk.MODE_FAST, 4, graph=graph)
+        got = self._run(lk, shape, lk.CS_TMA, lk.MODE_FAST, 4, graph=graph)
+        assert np.array_equal(got[2], ref[2]) and np.array_equal(got[3], ref[3])
+
+    def test_tma_singular_state_raises(self, lk):
+        shape = (128, 2, 4)
+        f0, g0 = _state(lk, shape, 1)
+        f0.data[:] = 0.0
+        prev = lk.cs_variant(lk.CS_TMA)
+        try:
+            with lk.BinaryFluid(lk.LatticeShape(*shape)) as sim:
+                sim.load(f0, g0)
+                sim.run(1)
+                with pytest.raises(lk.SingularStateError):
+                    sim.sync()
+        finally:
+            lk.cs_variant(prev)
+
+
 class TestSlabDecomposition:
     """P virtual slabs on one GPU, halos moved with the C-ABI face/plane calls."""
 
