@@ -384,11 +384,12 @@ def run_ours(args, rank, world, local):
     # ---------------- CPU baseline (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sample = (nx, ny, 16)
-        rate, threads, dt = cpu_oracle_rate(sample, 3, args.seed)
+        # bounded sample, ~10 s of CPU work on a 16-thread host (~10 MLUPS)
+        sample, csteps = (nx, ny, min(64, nzl)), 24
+        rate, threads, dt = cpu_oracle_rate(sample, csteps, args.seed)
         cpu = {"value": rate, "unit": "MLUPS", "cores": threads, "kind": "port",
-               "sample": f"{sample[0]}x{sample[1]}x{sample[2]} periodic lattice, 3 timesteps "
-                         f"({dt:.1f} s), oracle/lb_oracle.c orc_fluid_step"}
+               "sample": f"{sample[0]}x{sample[1]}x{sample[2]} periodic lattice, {csteps} "
+                         f"timesteps ({dt:.1f} s), oracle/lb_oracle.c orc_fluid_step"}
 
     sim.close()
     if rank == 0:
@@ -435,9 +436,11 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
     """Public-API path with host buffers, every step: H2D of the step's input
     state (f, g from pinned host memory) -> BinaryFluid load (on-device
     transpose to the slab layout) -> one timestep -> store (transpose back)
-    -> D2H of the result state.  Two staging buffers and three streams let the
-    H2D of step k+1 and the D2H of step k overlap the compute of the other
-    (PCIe is full duplex); every byte still crosses the bus every step."""
+    -> D2H of the result state.  Inputs and results have their own double-
+    buffered device staging, so the H2D stream (step k+1's input) and the D2H
+    stream (step k's result) each run back to back and overlap each other
+    and the compute (PCIe is full duplex); every byte still crosses the bus
+    every step."""
     nelem = f0.data.size
     nb = 8 * nelem
     from paper_1405_6162_b200.memory import pinned_empty
@@ -446,23 +449,23 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
     hf[:] = f0.data
     hg[:] = g0.data
     of, og = pinned_empty(nelem), pinned_empty(nelem)
-    stage = [nat.malloc(2 * nb), nat.malloc(2 * nb)]
+    stage_in = [nat.malloc(2 * nb), nat.malloc(2 * nb)]
+    stage_out = [nat.malloc(2 * nb), nat.malloc(2 * nb)]
     padded = f0.descriptor.padded_sites
     nzl = sim.nzl
     cs = sim.stream
     h2d_st, d2h_st = nat.stream_create(), nat.stream_create()
-    ev_in = [nat.event_create(), nat.event_create()]      # H2D of buffer b done
-    ev_loaded = [nat.event_create(), nat.event_create()]  # load consumed buffer b
-    ev_out = [nat.event_create(), nat.event_create()]     # store into buffer b done
-    ev_free = [nat.event_create(), nat.event_create()]    # D2H out of buffer b done
+    ev_in = [nat.event_create(), nat.event_create()]      # H2D into stage_in[b] done
+    ev_loaded = [nat.event_create(), nat.event_create()]  # load consumed stage_in[b]
+    ev_out = [nat.event_create(), nat.event_create()]     # store into stage_out[b] done
+    ev_free = [nat.event_create(), nat.event_create()]    # D2H out of stage_out[b] done
     chk = nat.check
     L = nat.lib
 
     def issue_h2d(b):
-        chk(L.ltk_stream_wait_event(h2d_st, ev_free[b]))
         chk(L.ltk_stream_wait_event(h2d_st, ev_loaded[b]))
-        chk(L.ltk_h2d(stage[b], hf.ctypes.data, nb, h2d_st))
-        chk(L.ltk_h2d(stage[b] + nb, hg.ctypes.data, nb, h2d_st))
+        chk(L.ltk_h2d(stage_in[b], hf.ctypes.data, nb, h2d_st))
+        chk(L.ltk_h2d(stage_in[b] + nb, hg.ctypes.data, nb, h2d_st))
         chk(L.ltk_event_record(ev_in[b], h2d_st))
 
     def run(nsteps):
@@ -475,14 +478,15 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
             if k + 1 < nsteps:
                 issue_h2d(1 - b)   # prefetch next step's input
             chk(L.ltk_stream_wait_event(cs, ev_in[b]))
-            sim.load_device(stage[b], stage[b] + nb, padded, nzl, 0, cs)
-            sim.run(1)
-            sim.store_device(stage[b], stage[b] + nb, padded, nzl, 0, cs)
-            chk(L.ltk_event_record(ev_out[b], cs))
+            sim.load_device(stage_in[b], stage_in[b] + nb, padded, nzl, 0, cs)
             chk(L.ltk_event_record(ev_loaded[b], cs))
+            sim.run(1)
+            chk(L.ltk_stream_wait_event(cs, ev_free[b]))   # result buffer drained
+            sim.store_device(stage_out[b], stage_out[b] + nb, padded, nzl, 0, cs)
+            chk(L.ltk_event_record(ev_out[b], cs))
             chk(L.ltk_stream_wait_event(d2h_st, ev_out[b]))
-            chk(L.ltk_d2h(of.ctypes.data, stage[b], nb, d2h_st))
-            chk(L.ltk_d2h(og.ctypes.data, stage[b] + nb, nb, d2h_st))
+            chk(L.ltk_d2h(of.ctypes.data, stage_out[b], nb, d2h_st))
+            chk(L.ltk_d2h(og.ctypes.data, stage_out[b] + nb, nb, d2h_st))
             chk(L.ltk_event_record(ev_free[b], d2h_st))
         chk(L.ltk_stream_wait_event(cs, ev_free[(nsteps - 1) & 1]))
 
@@ -496,8 +500,7 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
     sim.sync()
     ms = nat.elapsed_ms(start, stop)
     ms_max = ctl.allreduce(ms, "MAX")
-    # the last D2H result must equal a plain device run of the same input
-    for p in stage:
+    for p in stage_in + stage_out:
         nat.free(p)
     for s in (h2d_st, d2h_st):
         L.ltk_stream_destroy(s)
@@ -510,7 +513,8 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
             "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
             "steps": args.e2e_steps, "ms_per_step": ms_max / args.e2e_steps,
             "path": "pinned H2D(f,g) -> BinaryFluid.load_device -> run(1) -> store_device -> "
-                    "D2H(f,g); next step's H2D overlaps this step's D2H"}
+                    "D2H(f,g); separate double-buffered input/result staging, so step k+1's "
+                    "H2D and step k's D2H stream concurrently"}
 
 
 def main(argv=None):

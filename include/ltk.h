@@ -249,6 +249,14 @@ int ltk_fluid_set_fuse(ltk_fluid *e, int32_t enable, int32_t extra_lag);
 #define LTK_CS_REG 0
 #define LTK_CS_TMA 1
 int ltk_fluid_cs_variant(int32_t variant, int32_t *previous);
+/* Chemical-potential stencil kernel, process-wide: LTK_MU_AUTO = register
+ * 2.5-D column kernel k_mu_col (nx % 32 == 0, ny % 8 == 0), else the TMA
+ * shared-memory kernel k_mu_tma, else k_mu; LTK_MU_TMA skips k_mu_col;
+ * LTK_MU_PLAIN forces k_mu.  Bitwise identical.  variant < 0 only queries. */
+#define LTK_MU_AUTO 0
+#define LTK_MU_TMA 1
+#define LTK_MU_PLAIN 2
+int ltk_fluid_mu_variant(int32_t variant, int32_t *previous);
 /* Last step's per-kernel device times in ms (phi, mu, collide_stream, halo). */
 int ltk_fluid_profile(ltk_fluid *e, int32_t enable, float *ms4);
 

@@ -24,6 +24,7 @@ MODE_EXACT = 0
 MODE_FAST = 1
 CS_REG = 0
 CS_TMA = 1
+MU_AUTO, MU_TMA, MU_PLAIN = 0, 1, 2
 
 _ERRORS = {1: ConfigError, 2: BoundsError, 3: ShapeError, 4: AllocationError,
            5: LifecycleError, 6: PlanError, 7: DeviceError, 11: SingularStateError}
@@ -121,6 +122,7 @@ SIGNATURES = {
     "ltk_fluid_use_graph": (ctypes.c_int, [_vp, _i32]),
     "ltk_fluid_set_fuse": (ctypes.c_int, [_vp, _i32, _i32]),
     "ltk_fluid_cs_variant": (ctypes.c_int, [_i32, ctypes.POINTER(_i32)]),
+    "ltk_fluid_mu_variant": (ctypes.c_int, [_i32, ctypes.POINTER(_i32)]),
     "ltk_fluid_profile": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_float)]),
     "ltk_fluid_ipc_blob": (ctypes.c_int, [_vp, ctypes.c_char_p]),
     "ltk_fluid_attach_peers": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p]),

@@ -95,9 +95,24 @@ static int launch_phi(const FluidArgs &a, int vvl, cudaStream_t st) {
     return LTK_OK;
 }
 
+// mu stencil kernel (process-wide): LTK_MU_AUTO = k_mu_col where it applies,
+// else k_mu_tma, else k_mu; LTK_MU_TMA skips k_mu_col; LTK_MU_PLAIN = k_mu.
+static int &mu_variant() {
+    static int v = LTK_MU_AUTO;
+    return v;
+}
+
 static int launch_mu(const FluidArgs &a, int vvl, cudaStream_t st) {
     if (a.nthreads <= 0) return LTK_OK;
-    if (mu_tma_ok(a)) {
+    const int variant = mu_variant();
+    if (variant == LTK_MU_AUTO && mu_col_ok(a)) {
+        dim3 grid((unsigned)(a.nx / 32), (unsigned)(a.ny / 8),
+                  (unsigned)((a.nplanes + kMuColZ - 1) / kMuColZ));
+        k_mu_col<><<<grid, dim3(32, 8), 0, st>>>(a);
+        LTK_CHECK_LAUNCH("k_mu_col");
+        return LTK_OK;
+    }
+    if (variant != LTK_MU_PLAIN && mu_tma_ok(a)) {
         // shared-memory staged stencil, rows loaded by TMA bulk copies
         static bool attr_set = false;
         if (!attr_set) {
@@ -830,6 +845,7 @@ static int preload_step_kernels() {
     cudaFuncGetAttributes(&fa, k_mu<1>);
     cudaFuncGetAttributes(&fa, k_mu<2>);
     cudaFuncGetAttributes(&fa, k_mu<4>);
+    cudaFuncGetAttributes(&fa, k_mu_col<>);
     cudaFuncGetAttributes(&fa, k_mu_tma<4>);
     cudaFuncGetAttributes(&fa, k_mu_tma<2>);
     cudaFuncGetAttributes(&fa, k_plane_copy);
@@ -1412,6 +1428,15 @@ int ltk_fluid_cs_variant(int32_t variant, int32_t *previous) {
         if (variant != LTK_CS_REG && variant != LTK_CS_TMA)
             return fail(LTK_ERR_CONFIG, "unknown collide-stream variant %d", variant);
         cs_variant() = variant;
+    }
+    return LTK_OK;
+}
+
+int ltk_fluid_mu_variant(int32_t variant, int32_t *previous) {
+    if (previous) *previous = mu_variant();
+    if (variant >= 0) {
+        if (variant > LTK_MU_PLAIN) return fail(LTK_ERR_CONFIG, "unknown mu variant %d", variant);
+        mu_variant() = variant;
     }
     return LTK_OK;
 }

@@ -33,6 +33,7 @@ MODE_EXACT = nat.MODE_EXACT
 MODE_FAST = nat.MODE_FAST
 CS_REG = nat.CS_REG
 CS_TMA = nat.CS_TMA
+MU_AUTO, MU_TMA, MU_PLAIN = nat.MU_AUTO, nat.MU_TMA, nat.MU_PLAIN
 PHYSICS = {"passive": 0, "binary": 1}
 
 
@@ -315,6 +316,16 @@ def cs_variant(variant: int | None = None) -> int:
     prev = ctypes.c_int32(0)
     nat.check(nat.lib.ltk_fluid_cs_variant(-1 if variant is None else int(variant),
                                            ctypes.byref(prev)), "cs_variant")
+    return int(prev.value)
+
+
+def mu_variant(variant: int | None = None) -> int:
+    """Chemical-potential stencil kernel of the process: MU_AUTO (register
+    column kernel where it applies, else TMA, else plain), MU_TMA, MU_PLAIN.
+    Returns the previous value; None only queries."""
+    prev = ctypes.c_int32(0)
+    nat.check(nat.lib.ltk_fluid_mu_variant(-1 if variant is None else int(variant),
+                                           ctypes.byref(prev)), "mu_variant")
     return int(prev.value)
 
 
