@@ -49,11 +49,12 @@ template <int MODE>
 __device__ __forceinline__ void finish_site(Site &s, const CollideArgs &a) {
     if constexpr (MODE == LTK_MODE_EXACT) {
         using M = Exact;
-        s.ux = M::div(s.jx, s.rho);
-        s.uy = M::div(s.jy, s.rho);
-        s.uz = M::div(s.jz, s.rho);
+        const double rr = __drcp_rn(s.rho);  // RN(1/rho): three divisions by rho
+        s.ux = div_rcp(s.jx, s.rho, rr);
+        s.uy = div_rcp(s.jy, s.rho, rr);
+        s.uz = div_rcp(s.jz, s.rho, rr);
         double usq = M::add(M::add(M::mul(s.ux, s.ux), M::mul(s.uy, s.uy)), M::mul(s.uz, s.uz));
-        s.t = M::div(usq, a.c1);
+        s.t = div_rcp(usq, a.c1, a.a3);
     } else {
         double inv = 1.0 / s.rho;
         s.ux = s.jx * inv;
@@ -79,9 +80,9 @@ __device__ __forceinline__ void relax_exact(double &f, double &g, double q, doub
     const double geq = M::mul(M::mul(a.wv[I], s.phi), br);
     const double df = M::sub(f, feq), dg = M::sub(g, geq);
     if constexpr (T1 & 1) f = M::sub(f, df);  // x / 1.0 == x
-    else f = M::sub(f, M::div(df, a.tau_f));
+    else f = M::sub(f, div_rcp(df, a.tau_f, a.inv_tau_f));
     if constexpr (T1 & 2) g = M::sub(g, dg);
-    else g = M::sub(g, M::div(dg, a.tau_g));
+    else g = M::sub(g, div_rcp(dg, a.tau_g, a.inv_tau_g));
 }
 
 template <int I>
@@ -103,8 +104,8 @@ __device__ __forceinline__ void relax_pair(double (&F)[Q][W], double (&G)[Q][W],
     if constexpr (MODE == LTK_MODE_EXACT) {
         using M = Exact;
         const double ud = dot_c<cx(C), cy(C), cz(C), M>(s.ux, s.uy, s.uz);
-        const double q = M::div(ud, a.cs2);
-        const double sq = M::div(M::mul(ud, ud), a.c2);
+        const double q = div_rcp(ud, a.cs2, a.a1);
+        const double sq = div_rcp(M::mul(ud, ud), a.c2, a.a2);
         relax_exact<C, T1>(F[C][v], G[C][v], q, sq, s, a);
         if constexpr (O != C) relax_exact<O, T1>(F[O][v], G[O][v], -q, sq, s, a);
     } else {

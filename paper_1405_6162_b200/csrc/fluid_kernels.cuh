@@ -215,19 +215,21 @@ __device__ __forceinline__ void fsite_finish(FSite &s, double gmx, double gmy, d
             s.Fx = -M::mul(s.phi, gmx);
             s.Fy = -M::mul(s.phi, gmy);
             s.Fz = -M::mul(s.phi, gmz);
-            s.ux = M::div(M::add(s.jx, M::mul(0.5, s.Fx)), s.rho);
-            s.uy = M::div(M::add(s.jy, M::mul(0.5, s.Fy)), s.rho);
-            s.uz = M::div(M::add(s.jz, M::mul(0.5, s.Fz)), s.rho);
+            const double rr = __drcp_rn(s.rho);  // RN(1/rho): three divisions by rho
+            s.ux = div_rcp(M::add(s.jx, M::mul(0.5, s.Fx)), s.rho, rr);
+            s.uy = div_rcp(M::add(s.jy, M::mul(0.5, s.Fy)), s.rho, rr);
+            s.uz = div_rcp(M::add(s.jz, M::mul(0.5, s.Fz)), s.rho, rr);
             s.uF = M::add(M::add(M::mul(s.ux, s.Fx), M::mul(s.uy, s.Fy)), M::mul(s.uz, s.Fz));
             s.psi = M::sub(M::mul(a.gamma, s.mu), M::mul(s.phi, a.cs2));
         } else {
-            s.ux = M::div(s.jx, s.rho);
-            s.uy = M::div(s.jy, s.rho);
-            s.uz = M::div(s.jz, s.rho);
+            const double rr = __drcp_rn(s.rho);
+            s.ux = div_rcp(s.jx, s.rho, rr);
+            s.uy = div_rcp(s.jy, s.rho, rr);
+            s.uz = div_rcp(s.jz, s.rho, rr);
         }
         const double usq =
             M::add(M::add(M::mul(s.ux, s.ux), M::mul(s.uy, s.uy)), M::mul(s.uz, s.uz));
-        s.t = M::div(usq, a.c1);
+        s.t = div_rcp(usq, a.c1, a.a3);
     } else {
         const double inv = 1.0 / s.rho;
         if constexpr (PHYS == 1) {
@@ -264,20 +266,21 @@ __device__ __forceinline__ void frelax(double &f, double &g, double q, double sq
         const double df = M::sub(f, feq);
         double fn;
         if constexpr (T1 & 1) fn = M::sub(f, df);
-        else fn = M::sub(f, M::div(df, a.tau_f));
+        else fn = M::sub(f, div_rcp(df, a.tau_f, a.inv_tau_f));
         if constexpr (PHYS == 1) {
             const double ud = dot_c<cx(I), cy(I), cz(I), M>(s.ux, s.uy, s.uz);
             const double cF = dot_c<cx(I), cy(I), cz(I), M>(s.Fx, s.Fy, s.Fz);
             const double src =
                 M::mul(M::mul(a.srcpre, a.wv[I]),
-                       M::add(M::div(M::sub(cF, s.uF), a.cs2), M::div(M::mul(ud, cF), a.cs2sq)));
+                       M::add(div_rcp(M::sub(cF, s.uF), a.cs2, a.inv_cs2),
+                              div_rcp(M::mul(ud, cF), a.cs2sq, a.inv_cs2sq)));
             fn = M::add(fn, src);
             geq = M::add(geq, M::mul(a.lam[I], s.psi));
         }
         f = fn;
         const double dg = M::sub(g, geq);
         if constexpr (T1 & 2) g = M::sub(g, dg);
-        else g = M::sub(g, M::div(dg, a.tau_g));
+        else g = M::sub(g, div_rcp(dg, a.tau_g, a.inv_tau_g));
     } else {
         const double ud = dot_c<cx(I), cy(I), cz(I), Fast>(s.ux, s.uy, s.uz);
         const double br = fma(ud, fma(ud, a.a2, a.a1), s.t);
@@ -305,8 +308,8 @@ __device__ __forceinline__ void frelax_pair(double (&F)[Q][VVL], double (&G)[Q][
     if constexpr (MODE == LTK_MODE_EXACT) {
         using M = Exact;
         const double ud = dot_c<cx(C), cy(C), cz(C), M>(s.ux, s.uy, s.uz);
-        q = M::div(ud, a.cs2);
-        sq = M::div(M::mul(ud, ud), a.c2);
+        q = div_rcp(ud, a.cs2, a.a1);
+        sq = div_rcp(M::mul(ud, ud), a.c2, a.a2);
     }
     frelax<C, MODE, PHYS, T1>(F[C][k], G[C][k], q, sq, s, a);
     if constexpr (O != C) frelax<O, MODE, PHYS, T1>(F[O][k], G[O][k], -q, sq, s, a);

@@ -113,6 +113,22 @@ struct Exact {
     __device__ static __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
 };
 
+// Correctly rounded x / d from r = RN(1/d) (Markstein's theorem; Muller et
+// al., Handbook of Floating-Point Arithmetic): q = RN(x r) is a faithful
+// quotient because r has relative error < 2^-53, the remainder e = x - d q is
+// exact in one FMA, and RN(q + e r) == RN(x / d) whenever nothing overflows or
+// underflows.  So this is bitwise __ddiv_rn(x, d) for the lattice's operands
+// in 3 dependent FP64 ops instead of the ~10-op, branchy division sequence.
+// Edge cases (d > 0 finite everywhere here): a zero quotient keeps the sign of
+// x (x is then +-0), an infinite x passes through, NaN stays NaN.
+__device__ __forceinline__ double div_rcp(double x, double d, double r) {
+    const double q = __dmul_rn(x, r);
+    const double e = __fma_rn(-q, d, x);
+    double res = __fma_rn(e, r, q);
+    if (res == 0.0 || isinf(x)) res = x;
+    return res;
+}
+
 // FAST: plain operators (the compiler may contract to FMA).
 struct Fast {
     static constexpr bool exact = false;

@@ -122,12 +122,14 @@ class TestFullStepParity:
             with pytest.raises(lk.SingularStateError):
                 sim.sync()
 
-    def test_nccl_self_exchange_matches_wrap(self, lk):
+    @pytest.mark.parametrize("fuse", [False, True])
+    def test_nccl_self_exchange_matches_wrap(self, lk, fuse):
         if not lk.nccl_available():
             pytest.skip("libnccl.so.2 not loadable")
         shape = (16, 8, 8)
         f0, g0 = _state(lk, shape, 13)
         with lk.BinaryFluid(lk.LatticeShape(*shape), use_graph=False) as sim:
+            sim.set_fuse(fuse, 0)
             sim.attach_nccl(lk.nccl_unique_id())
             sim.load(f0, g0)
             sim.run(3)

@@ -90,19 +90,24 @@ def _worker(rank, world, port, shape, steps, physics, q):
         dist.destroy_process_group()
 
 
+# variant: "plain" (three-kernel step), "fused" (k_cs_phi on the interior planes
+# of every slab; needs nzl >= 5), "tma" (k_cs_tma; nx a multiple of 128)
 @pytest.mark.parametrize("nslabs", [2, 3, 4])
 @pytest.mark.parametrize("physics", ["binary", "passive"])
-@pytest.mark.parametrize("nz", [12, 24])  # nz 24: every slab runs the fused k_cs_phi interior
-def test_engines_in_one_process_bitwise(nslabs, physics, nz):
+@pytest.mark.parametrize("nz,variant", [(12, "plain"), (24, "plain"), (24, "fused"), (24, "tma")])
+def test_engines_in_one_process_bitwise(nslabs, physics, nz, variant):
     import paper_1405_6162_b200 as lk
     from oracle import oracle as orc
     from paper_1405_6162_b200.kernels import random_binary_state
 
-    shape, steps = (32, 8, nz), 4
+    shape, steps = ((128, 4, nz) if variant == "tma" else (32, 8, nz)), 4
     full = lk.LatticeShape(*shape)
     model = lk.D3Q19Model(tau_f=0.9, tau_g=1.1)
+    prev = lk.cs_variant(lk.CS_TMA if variant == "tma" else lk.CS_REG)
     sims = [lk.BinaryFluid(full, model=model, physics=physics, rank=r, nranks=nslabs,
                            use_graph=False) for r in range(nslabs)]
+    for sim in sims:
+        sim.set_fuse(variant == "fused", 1)
     try:
         for r, sim in enumerate(sims):
             sim.attach_peer_engines(sims[(r + 1) % nslabs], sims[(r - 1) % nslabs])
@@ -123,6 +128,7 @@ def test_engines_in_one_process_bitwise(nslabs, physics, nz):
     finally:
         for sim in sims:
             sim.close()
+        lk.cs_variant(prev)
     nx, ny, nz = shape
     nzl = nz // nslabs
     got = [np.concatenate([p[k].components()[:, :nx * ny * nzl].reshape(19, nx, ny, nzl)
