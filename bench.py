@@ -73,6 +73,8 @@ def parse_args(argv=None):
                         "one global lattice split into z-slabs")
     p.add_argument("--mode", choices=("exact", "fast"), default="fast")
     p.add_argument("--vvl", type=int, default=1)
+    p.add_argument("--tau", type=float, default=1.0,
+                   help="tau_f = tau_g (reference default 1.0, model.py:48-49)")
     p.add_argument("--e2e-steps", type=int, default=16)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -306,7 +308,7 @@ def run_ours(args, rank, world, local):
         nzl = nz_arg
     shape = lk.LatticeShape(nx, ny, nzl * world)
     mode = lk.MODE_FAST if args.mode == "fast" else lk.MODE_EXACT
-    model = lk.D3Q19Model(tau_f=1.0, tau_g=1.0)
+    model = lk.D3Q19Model(tau_f=args.tau, tau_g=args.tau)
     sim = lk.BinaryFluid(shape, model=model, physics="binary", mode=mode, vvl=args.vvl,
                          rank=rank, nranks=world, device=local, use_graph=False)
     fused = args.fuse
@@ -408,7 +410,8 @@ def run_ours(args, rank, world, local):
                                     "(BASELINE configs[3], strong scaling)"),
                        "lattice": f"{nx}x{ny}x{nzl * world}",
                        "shape_per_gpu": f"{nx}x{ny}x{nzl}",
-                       "mode": args.mode, "vvl": args.vvl, "physics": "binary free energy",
+                       "mode": args.mode, "vvl": args.vvl, "tau": args.tau,
+                       "physics": "binary free energy",
                        "fused": fused, "fuse_lag": args.fuse_lag if fused else None,
                        "l2": f"state {4 * 19 * 8 * nx * ny * nzl / 1e9:.1f} GB/GPU >> 126 MB L2, "
                              "no flush needed",

@@ -138,6 +138,12 @@ int ltk_collide(int64_t chunk_lo, int64_t chunk_hi, int32_t vvl, int32_t tpb, do
 
 /* Masked transfers (memory.py:277-315): component-major pack of the k sites
  * listed in idx (device int64[k]) into packed[ncomp*k], and the inverse. */
+/* Diagnostics: the EXACT-mode division (x * RN(1/d) with one FMA residual
+ * correction, Markstein) next to the hardware IEEE division, element-wise
+ * over device arrays x[n], d[n] (d > 0).  Test infrastructure for the claim
+ * that EXACT mode stays bitwise equal to the reference's true divisions. */
+int ltk_div_selftest(const double *x, const double *d, int64_t n, double *out_rcp,
+                     double *out_div, void *stream);
 int ltk_pack_sites(const double *src, double *packed, const int64_t *idx, int64_t k,
                    int32_t ncomp, int64_t padded, void *stream);
 int ltk_unpack_sites(double *dst, const double *packed, const int64_t *idx, int64_t k,

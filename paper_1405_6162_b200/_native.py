@@ -122,6 +122,7 @@ SIGNATURES = {
     "ltk_fluid_use_graph": (ctypes.c_int, [_vp, _i32]),
     "ltk_fluid_set_fuse": (ctypes.c_int, [_vp, _i32, _i32]),
     "ltk_fluid_cs_variant": (ctypes.c_int, [_i32, ctypes.POINTER(_i32)]),
+    "ltk_div_selftest": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
     "ltk_fluid_mu_variant": (ctypes.c_int, [_i32, ctypes.POINTER(_i32)]),
     "ltk_fluid_profile": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_float)]),
     "ltk_fluid_ipc_blob": (ctypes.c_int, [_vp, ctypes.c_char_p]),

@@ -291,3 +291,25 @@ extern "C" int ltk_scale(int64_t chunk_lo, int64_t chunk_hi, int32_t vvl, int32_
     LTK_CHECK_LAUNCH("k_scale");
     return LTK_OK;
 }
+
+// Self-test of div_rcp (the EXACT division path) against the hardware
+// division: out_rcp[k] = div_rcp(x, d, RN(1/d)), out_div[k] = __ddiv_rn(x, d).
+__global__ void k_div_selftest(const double *x, const double *d, long long n, double *out_rcp,
+                               double *out_div) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (long long)gridDim.x * blockDim.x) {
+        const double r = __drcp_rn(d[k]);
+        out_rcp[k] = ltk::div_rcp(x[k], d[k], r);
+        out_div[k] = __ddiv_rn(x[k], d[k]);
+    }
+}
+
+extern "C" int ltk_div_selftest(const double *x, const double *d, int64_t n, double *out_rcp,
+                                double *out_div, void *stream) {
+    if (n <= 0) return LTK_OK;
+    const long long blocks = (n + 255) / 256;
+    const unsigned g = (unsigned)(blocks < 148LL * 8 ? blocks : 148LL * 8);
+    k_div_selftest<<<g, 256, 0, ltk::as_stream(stream)>>>(x, d, n, out_rcp, out_div);
+    LTK_CHECK_LAUNCH("k_div_selftest");
+    return LTK_OK;
+}

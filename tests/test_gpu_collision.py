@@ -361,3 +361,47 @@ class TestStress:
             assert sha(f1.data) == case["out_f"] and sha(g1.data) == case["out_g"], (k, vvl, tpb)
             if k % 10 == 0:
                 run_framework_collision(big_f, big_g, "cuda", 2, 1, steps=1, model=model)
+
+
+class TestExactDivision:
+    """EXACT mode divides by launch constants and by rho through precomputed
+    reciprocals (ltk_common.cuh div_rcp, Markstein's theorem).  Checked here
+    against the hardware IEEE division on operands spanning the normal
+    exponent range, plus signed zeros, infinities and NaN: bitwise equal
+    wherever the quotient and the residual stay normal."""
+
+    def test_div_rcp_equals_ieee_division(self, lk):
+        from paper_1405_6162_b200 import _native as nat
+
+        rng = np.random.default_rng(20141406)
+        n = 4_000_000
+        x = rng.uniform(1.0, 2.0, n) * np.exp2(rng.integers(-480, 480, n)) * \
+            rng.choice([-1.0, 1.0], n)
+        d = rng.uniform(1.0, 2.0, n) * np.exp2(rng.integers(-480, 480, n))
+        # the constants EXACT mode divides by, and lattice-scale operands
+        consts = np.array([1 / 3, 2 / 3, 2 / 9, 1 / 9, 0.8, 0.9, 1.1, 1.3, 0.51, 1.0])
+        d[: n // 4] = rng.choice(consts, n // 4)
+        x[: n // 4] = rng.standard_normal(n // 4) * np.exp2(rng.integers(-60, 4, n // 4))
+        # rho-like divisors (near 1) with momentum-like numerators
+        d[n // 4: n // 2] = 1.0 + 0.2 * rng.random(n // 4)
+        x[n // 4: n // 2] = rng.standard_normal(n // 4) * 1e-3
+        specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-300, -3e-290, 5e300])
+        x[-len(specials):] = specials
+        d[-len(specials):] = 0.8
+        buf = [nat.malloc(8 * n) for _ in range(4)]
+        try:
+            nat.check(nat.lib.ltk_h2d(buf[0], x.ctypes.data, 8 * n, None))
+            nat.check(nat.lib.ltk_h2d(buf[1], d.ctypes.data, 8 * n, None))
+            nat.check(nat.lib.ltk_div_selftest(buf[0], buf[1], n, buf[2], buf[3], None))
+            got, ref = np.empty(n), np.empty(n)
+            nat.check(nat.lib.ltk_d2h(got.ctypes.data, buf[2], 8 * n, None))
+            nat.check(nat.lib.ltk_d2h(ref.ctypes.data, buf[3], 8 * n, None))
+            nat.check(nat.lib.ltk_stream_sync(None))
+        finally:
+            for b in buf:
+                nat.free(b)
+        assert np.array_equal(ref, x / d, equal_nan=True)   # the device IEEE division is numpy's
+        nan = np.isnan(ref)
+        assert np.array_equal(np.isnan(got), nan)
+        same = got[~nan].view(np.uint64) == ref[~nan].view(np.uint64)
+        assert same.all(), (x[~nan][~same][:5], d[~nan][~same][:5])
