@@ -298,6 +298,11 @@ def run_ours(args, rank, world, local):
     from paper_1405_6162_b200.kernels import random_binary_state
 
     ctl = Control(world)
+    ndev = nat.device_count()
+    if local >= ndev:  # more ranks than GPUs (testing): ranks share devices round-robin
+        print(f"warning: rank {rank} shares device {local % ndev} ({ndev} visible)",
+              file=sys.stderr)
+        local = local % ndev
     nat.check(nat.lib.ltk_set_device(local))
     nx, ny, nz_arg = (int(v) for v in args.shape.lower().split("x"))
     if args.scaling == "strong":

@@ -141,8 +141,6 @@ def test_engines_in_one_process_bitwise(nslabs, physics, nz, variant):
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-@pytest.mark.skip(reason="two CUDA processes sharing the one GPU of the test box corrupt "
-                         "plain memcpys (scripts/debug_peer4.py); needs one GPU per process")
 @pytest.mark.parametrize("physics", ["binary", "passive"])
 def test_two_process_peer_slabs_bitwise(physics):
     import torch.multiprocessing as mp
