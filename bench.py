@@ -6,8 +6,11 @@
 Workload (BASELINE.json configs[2], and configs[4] at N > 1): one full
 timestep = pull streaming + order parameter phi + chemical potential mu
 (7-point stencil) + Guo-forced binary collision, fp64, periodic, 256^3 sites
-per GPU (weak scaling: z-slabs of 256 planes per rank, NCCL halos).  A "step"
-is one timestep of the whole lattice.  Inputs: reference random_binary_state
+per GPU (weak scaling: z-slabs of 256 planes per rank, halos stored by the
+kernels into the neighbours over NVLink, or NCCL).  A "step" is one timestep
+of the whole lattice, in EXACT arithmetic by default (bitwise equal to the
+oracle / reference op order; --mode fast for FMA arithmetic within 1e-12).
+Inputs: reference random_binary_state
 per slab (kernels.py:216-227), synthetic.  State (2 x 2 x 2.55 GB per GPU) is
 far larger than L2, so no L2 flush is needed between steps.
 
@@ -71,7 +74,9 @@ def parse_args(argv=None):
     p.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                    help="weak: BASELINE configs[2]/[4], 256^3 per GPU; strong: configs[3], "
                         "one global lattice split into z-slabs")
-    p.add_argument("--mode", choices=("exact", "fast"), default="fast")
+    p.add_argument("--mode", choices=("exact", "fast"), default="exact",
+                   help="exact: bitwise equal to the reference arithmetic (default); fast: "
+                        "FMA/reciprocal arithmetic within 1e-12")
     p.add_argument("--vvl", type=int, default=1)
     p.add_argument("--tau", type=float, default=1.0,
                    help="tau_f = tau_g (reference default 1.0, model.py:48-49)")

@@ -712,7 +712,7 @@ __global__ void k_peer_wait(const unsigned long long *inbox, unsigned long long 
                             int *timeout) {
     long long spins = 0;
     while (ld_acquire_sys(inbox) < target || ld_acquire_sys(inbox + 1) < target) {
-        if (++spins > (1LL << 28)) {  // never hang the GPU: record and go on
+        if (++spins > (1LL << 25)) {  // never hang the GPU (~10 s): record and go on
             atomicExch(timeout, 1);
             break;
         }
