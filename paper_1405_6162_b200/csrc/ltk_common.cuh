@@ -121,12 +121,16 @@ struct Exact {
 // in 3 dependent FP64 ops instead of the ~10-op, branchy division sequence.
 // Edge cases (d > 0 finite everywhere here): a zero quotient keeps the sign of
 // x (x is then +-0), an infinite x passes through, NaN stays NaN.
+// The guard tests x's bit pattern on the integer pipe (exponent all ones:
+// inf/NaN -> x; all bits but the sign zero: +-0 -> x) so the division costs
+// exactly three FP64-pipe instructions.
 __device__ __forceinline__ double div_rcp(double x, double d, double r) {
     const double q = __dmul_rn(x, r);
     const double e = __fma_rn(-q, d, x);
-    double res = __fma_rn(e, r, q);
-    if (res == 0.0 || isinf(x)) res = x;
-    return res;
+    const double res = __fma_rn(e, r, q);
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const bool pass = ((b >> 52) & 0x7ffull) == 0x7ffull || (b << 1) == 0ull;
+    return pass ? x : res;
 }
 
 // FAST: plain operators (the compiler may contract to FMA).

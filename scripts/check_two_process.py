@@ -1,3 +1,5 @@
+"""Two CUDA processes on one GPU: H2D round trip and slab scatter per process (the
+cross-process check behind tests/test_gpu_peer.py::test_two_process_*)."""
 import os, sys, socket, ctypes, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
