@@ -177,10 +177,9 @@ __device__ __forceinline__ void cs_ldgsts_issue(const FluidArgs &a, const TileXY
 // STAGES * stage_bytes.  Tile j goes to CTA j mod grid; no inter-CTA
 // dependencies.  Consumers are scheduled per 32-site chunk: consumer warp w
 // takes chunks w, w + NCW, ... of the CTA's chunk sequence (TX/32 chunks per
-// tile), so any number of consumer warps can share the ring.  A warp's stride
-// is NCW/(TX/32) tiles < STAGES, so it never waits on a stage two fills ahead
-// (mbarrier parity stays unambiguous).  Requires nx % TX == 0 (FULL: nx == TX)
-// and VVL == 1.
+// tile), so any number of consumer warps can share the ring; slot_tile keeps
+// their barrier waits unambiguous.  Requires nx % TX == 0 (FULL: nx == TX) and
+// VVL == 1.
 template <int MODE, int PHYS, int T1, int TX, bool FULL, int STAGES, int NCW, int NPW>
 __global__ void __launch_bounds__(32 * ((NPW > 0 ? NPW : 1) + NCW), 1) k_cs_tma(const FluidArgs a) {
     // NPW == 0: one TMA producer warp; NPW > 0: NPW LDGSTS producer warps
@@ -190,11 +189,20 @@ __global__ void __launch_bounds__(32 * ((NPW > 0 ? NPW : 1) + NCW), 1) k_cs_tma(
     static_assert(NCW < STAGES * WPT, "consumer stride must stay below the ring depth");
     extern __shared__ __align__(128) double stage[];
     __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+    // slot_tile[s]: the CTA-local tile index k whose copies slot s is receiving
+    // (written by the producer after the slot's previous tile was released).
+    // mbarrier waits test a 1-bit phase parity against the current or the
+    // immediately preceding phase only, and a consumer warp whose stride
+    // exceeds one tile may reach slot s while the slot's previous fill is still
+    // in flight -- the parity of its phase would alias the phase before that.
+    // Waiting for the tag first pins the barrier to this tile's phase.
+    __shared__ volatile long long slot_tile[STAGES];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], NPW > 0 ? 32 * NPW : 1);
             mbar_init(&empty[s], WPT);
+            slot_tile[s] = -1;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -207,6 +215,8 @@ __global__ void __launch_bounds__(32 * ((NPW > 0 ? NPW : 1) + NCW), 1) k_cs_tma(
         for (long long j = blockIdx.x; j < ntiles; j += G, ++k) {
             const int s = (int)(k % STAGES);
             if (k >= STAGES) mbar_wait(&empty[s], (uint32_t)((k / STAGES - 1) & 1));
+            if (threadIdx.x == 0) slot_tile[s] = k;  // before the barrier is armed
+            __syncwarp();
             double *sb = stage + (size_t)s * (Gm::stage_bytes / 8);
             if constexpr (NPW == 0) {
                 if (lane == 0) mbar_expect_tx(&full[s], Gm::tile_bytes);
@@ -227,6 +237,7 @@ __global__ void __launch_bounds__(32 * ((NPW > 0 ? NPW : 1) + NCW), 1) k_cs_tma(
         const int xl = (int)(q % WPT) * 32 + lane;
         const long long j = blockIdx.x + k * G;
         const int s = (int)(k % STAGES);
+        while (slot_tile[s] != k) __nanosleep(32);  // the slot now receives tile k
         mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
         const double *sb = stage + (size_t)s * (Gm::stage_bytes / 8);
         double F[Q][1], G_[Q][1];

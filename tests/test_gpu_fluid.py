@@ -236,6 +236,17 @@ class TestTmaCollideStream:
         got = self._run(lk, shape, lk.CS_TMA, lk.MODE_FAST, 4, graph=graph)
         assert np.array_equal(got[2], ref[2]) and np.array_equal(got[3], ref[3])
 
+    def test_tma_long_ring_equals_register_kernel(self, lk):
+        # ~110 tiles per CTA: every stage slot is refilled many times, so a
+        # consumer warp regularly reaches a slot whose previous fill is still in
+        # flight (the mbarrier parity-aliasing case slot_tile guards against).
+        # Bitwise equal to the register kernel and deterministic across runs.
+        shape = (256, 256, 64)
+        ref = self._run(lk, shape, lk.CS_REG, lk.MODE_FAST, 3)
+        for _ in range(2):
+            got = self._run(lk, shape, lk.CS_TMA, lk.MODE_FAST, 3)
+            assert np.array_equal(got[2], ref[2]) and np.array_equal(got[3], ref[3])
+
     def test_tma_singular_state_raises(self, lk):
         shape = (128, 2, 4)
         f0, g0 = _state(lk, shape, 1)
