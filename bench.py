@@ -257,8 +257,8 @@ def cpu_oracle_rate(shape, steps, seed, threads=None):
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
-    nx, ny, _ = (int(v) for v in args.shape.lower().split("x"))
-    sample = (nx, ny, 32)
+    nx, ny, nz = (int(v) for v in args.shape.lower().split("x"))
+    sample = (nx, ny, min(64, nz))  # the cpu_baseline sample of our arm
     steps = max(1, args.steps)
     from oracle import oracle as orc
 
