@@ -8,11 +8,12 @@ import paper_1405_6162_b200 as lk
 from paper_1405_6162_b200 import _native as nat
 from paper_1405_6162_b200.kernels import random_binary_state
 
+MODE = lk.MODE_FAST if "--fast" in sys.argv else lk.MODE_EXACT  # bench default: EXACT
 full = lk.LatticeShape(256, 256, 256)
 f0, g0 = random_binary_state(full, np.random.default_rng(1234))
 res = {}
 for P in (1, 2, 4, 8):
-    sims = [lk.BinaryFluid(full, mode=lk.MODE_FAST, rank=r, nranks=P, use_graph=(P == 1))
+    sims = [lk.BinaryFluid(full, mode=MODE, rank=r, nranks=P, use_graph=(P == 1))
             for r in range(P)]
     if P > 1:
         for r, sim in enumerate(sims):
@@ -49,7 +50,7 @@ for P in (1, 2, 4, 8):
         sim.close()
 
 if lk.nccl_available():
-    sim = lk.BinaryFluid(full, mode=lk.MODE_FAST, use_graph=False)
+    sim = lk.BinaryFluid(full, mode=MODE, use_graph=False)
     sim.attach_nccl(lk.nccl_unique_id())
     sim.load(f0, g0); sim.run(3); sim.sync()
     s, e = nat.event_create(True), nat.event_create(True)
