@@ -80,7 +80,11 @@ def parse_args(argv=None):
     p.add_argument("--vvl", type=int, default=1)
     p.add_argument("--tau", type=float, default=1.0,
                    help="tau_f = tau_g (reference default 1.0, model.py:48-49)")
-    p.add_argument("--e2e-steps", type=int, default=16)
+    p.add_argument("--e2e-steps", type=int, default=48,
+                   help="e2e steps (pipeline fill/drain of one H2D + one D2H is amortised "
+                        "over them)")
+    p.add_argument("--e2e-streams", type=int, choices=(1, 2), default=1,
+                   help="copy streams per PCIe direction in the e2e path")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=1234)
@@ -467,41 +471,50 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
     padded = f0.descriptor.padded_sites
     nzl = sim.nzl
     cs = sim.stream
-    h2d_st, d2h_st = nat.stream_create(), nat.stream_create()
-    ev_in = [nat.event_create(), nat.event_create()]      # H2D into stage_in[b] done
+    # f and g copies on one stream per direction, or on two (--e2e-streams 2)
+    h2d_st = [nat.stream_create()] * 2
+    d2h_st = [nat.stream_create()] * 2
+    if args.e2e_streams == 2:
+        h2d_st[1], d2h_st[1] = nat.stream_create(), nat.stream_create()
+    ev_in = [[nat.event_create(), nat.event_create()] for _ in range(2)]    # [b][f/g] H2D done
     ev_loaded = [nat.event_create(), nat.event_create()]  # load consumed stage_in[b]
     ev_out = [nat.event_create(), nat.event_create()]     # store into stage_out[b] done
-    ev_free = [nat.event_create(), nat.event_create()]    # D2H out of stage_out[b] done
+    ev_free = [[nat.event_create(), nat.event_create()] for _ in range(2)]  # [b][f/g] D2H done
     chk = nat.check
     L = nat.lib
+    host_in, host_out = (hf, hg), (of, og)
 
     def issue_h2d(b):
-        chk(L.ltk_stream_wait_event(h2d_st, ev_loaded[b]))
-        chk(L.ltk_h2d(stage_in[b], hf.ctypes.data, nb, h2d_st))
-        chk(L.ltk_h2d(stage_in[b] + nb, hg.ctypes.data, nb, h2d_st))
-        chk(L.ltk_event_record(ev_in[b], h2d_st))
+        for c in (0, 1):
+            chk(L.ltk_stream_wait_event(h2d_st[c], ev_loaded[b]))
+            chk(L.ltk_h2d(stage_in[b] + c * nb, host_in[c].ctypes.data, nb, h2d_st[c]))
+            chk(L.ltk_event_record(ev_in[b][c], h2d_st[c]))
 
     def run(nsteps):
         for b in (0, 1):
-            chk(L.ltk_event_record(ev_free[b], d2h_st))
+            for c in (0, 1):
+                chk(L.ltk_event_record(ev_free[b][c], d2h_st[c]))
             chk(L.ltk_event_record(ev_loaded[b], cs))
         issue_h2d(0)
         for k in range(nsteps):
             b = k & 1
             if k + 1 < nsteps:
                 issue_h2d(1 - b)   # prefetch next step's input
-            chk(L.ltk_stream_wait_event(cs, ev_in[b]))
+            for c in (0, 1):
+                chk(L.ltk_stream_wait_event(cs, ev_in[b][c]))
             sim.load_device(stage_in[b], stage_in[b] + nb, padded, nzl, 0, cs)
             chk(L.ltk_event_record(ev_loaded[b], cs))
             sim.run(1)
-            chk(L.ltk_stream_wait_event(cs, ev_free[b]))   # result buffer drained
+            for c in (0, 1):
+                chk(L.ltk_stream_wait_event(cs, ev_free[b][c]))   # result buffer drained
             sim.store_device(stage_out[b], stage_out[b] + nb, padded, nzl, 0, cs)
             chk(L.ltk_event_record(ev_out[b], cs))
-            chk(L.ltk_stream_wait_event(d2h_st, ev_out[b]))
-            chk(L.ltk_d2h(of.ctypes.data, stage_out[b], nb, d2h_st))
-            chk(L.ltk_d2h(og.ctypes.data, stage_out[b] + nb, nb, d2h_st))
-            chk(L.ltk_event_record(ev_free[b], d2h_st))
-        chk(L.ltk_stream_wait_event(cs, ev_free[(nsteps - 1) & 1]))
+            for c in (0, 1):
+                chk(L.ltk_stream_wait_event(d2h_st[c], ev_out[b]))
+                chk(L.ltk_d2h(host_out[c].ctypes.data, stage_out[b] + c * nb, nb, d2h_st[c]))
+                chk(L.ltk_event_record(ev_free[b][c], d2h_st[c]))
+        for c in (0, 1):
+            chk(L.ltk_stream_wait_event(cs, ev_free[(nsteps - 1) & 1][c]))
 
     run(1)
     sim.sync()
@@ -515,7 +528,7 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
     ms_max = ctl.allreduce(ms, "MAX")
     for p in stage_in + stage_out:
         nat.free(p)
-    for s in (h2d_st, d2h_st):
+    for s in set(h2d_st + d2h_st):
         L.ltk_stream_destroy(s)
     from paper_1405_6162_b200.memory import pinned_free
 
@@ -527,7 +540,8 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
             "steps": args.e2e_steps, "ms_per_step": ms_max / args.e2e_steps,
             "path": "pinned H2D(f,g) -> BinaryFluid.load_device -> run(1) -> store_device -> "
                     "D2H(f,g); separate double-buffered input/result staging, so step k+1's "
-                    "H2D and step k's D2H stream concurrently"}
+                    "H2D and step k's D2H stream concurrently; "
+                    "timed steps include the pipeline fill (first H2D) and drain (last D2H)"}
 
 
 def main(argv=None):
