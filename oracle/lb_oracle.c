@@ -23,6 +23,7 @@
  * The exact formulas and op order are written out in DESIGN.md §2.
  */
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 #include <math.h>
 #ifdef _OPENMP
@@ -145,7 +146,9 @@ typedef struct {
     double lam[Q];
     double cs2, tau_f, tau_g;
     double A, B, kappa, gamma;
-    int32_t physics; /* 0 = passive (reference collision), 1 = free-energy binary fluid */
+    int32_t physics; /* 0 = passive (reference collision), 1 = free-energy binary fluid
+                      * with F = -phi grad(mu), 2 = same fluid with the momentum-conserving
+                      * force F = -div P (chemical pressure tensor) */
     int32_t pad_;
 } orc_fluid_params;
 
@@ -205,9 +208,72 @@ void orc_mu(const double *phi, double *mu, int64_t nx, int64_t ny, int64_t nz,
             }
 }
 
+/* Chemical pressure tensor of the symmetric free energy (physics 2):
+ *   P_ab = p_iso delta_ab + kappa d_a phi d_b phi,
+ *   p_iso = (phi mu - (A/2 phi^2 + B/4 phi^4)) - kappa/2 |grad phi|^2,
+ * so that div P = phi grad mu in the continuum.  Per site this writes p_iso and
+ * the central gradient (gx, gy, gz) of phi; mu must be orc_mu's.  Op order:
+ *   g_a = (phi(+a) - phi(-a)) * 0.5,  gsq = ((gx gx) + (gy gy)) + (gz gz),
+ *   pp = phi phi,  fb = ((0.5 A) pp) + ((0.25 B) (pp pp)),
+ *   p_iso = ((phi mu) - fb) - ((0.5 kappa) gsq). */
+void orc_stress(const double *phi, const double *mu, double *piso, double *gx, double *gy,
+                double *gz, int64_t nx, int64_t ny, int64_t nz, double A, double B, double kappa)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t x = 0; x < nx; ++x)
+        for (int64_t y = 0; y < ny; ++y)
+            for (int64_t z = 0; z < nz; ++z) {
+                const int64_t s = site_of(x, y, z, ny, nz);
+                const double p = phi[s];
+                const double ax = (phi[site_of(wrap(x + 1, nx), y, z, ny, nz)] -
+                                   phi[site_of(wrap(x - 1, nx), y, z, ny, nz)]) * 0.5;
+                const double ay = (phi[site_of(x, wrap(y + 1, ny), z, ny, nz)] -
+                                   phi[site_of(x, wrap(y - 1, ny), z, ny, nz)]) * 0.5;
+                const double az = (phi[site_of(x, y, wrap(z + 1, nz), ny, nz)] -
+                                   phi[site_of(x, y, wrap(z - 1, nz), ny, nz)]) * 0.5;
+                const double gsq = ((ax * ax) + (ay * ay)) + (az * az);
+                const double pp = p * p;
+                const double fb = ((0.5 * A) * pp) + ((0.25 * B) * (pp * pp));
+                piso[s] = ((p * mu[s]) - fb) - ((0.5 * kappa) * gsq);
+                gx[s] = ax;
+                gy[s] = ay;
+                gz[s] = az;
+            }
+}
+
+/* F_a = -((D_x P_ax + D_y P_ay) + D_z P_az) at site (x, y, z), D_b h =
+ * (h(+b) - h(-b)) * 0.5, P_aa = p_iso + ((kappa g_a) g_a), P_ab = (kappa g_a) g_b:
+ * a discrete divergence, so sum_x F = 0 up to rounding (momentum conserved). */
+static void stress_force(const double *piso, const double *const g[3], double kappa, int64_t x,
+                         int64_t y, int64_t z, int64_t nx, int64_t ny, int64_t nz, double F[3])
+{
+    int64_t sp[3], sm[3];
+    sp[0] = site_of(wrap(x + 1, nx), y, z, ny, nz);
+    sm[0] = site_of(wrap(x - 1, nx), y, z, ny, nz);
+    sp[1] = site_of(x, wrap(y + 1, ny), z, ny, nz);
+    sm[1] = site_of(x, wrap(y - 1, ny), z, ny, nz);
+    sp[2] = site_of(x, y, wrap(z + 1, nz), ny, nz);
+    sm[2] = site_of(x, y, wrap(z - 1, nz), ny, nz);
+    for (int a = 0; a < 3; ++a) {
+        double d[3];
+        for (int b = 0; b < 3; ++b) {
+            double tp = (kappa * g[a][sp[b]]) * g[b][sp[b]];
+            double tm = (kappa * g[a][sm[b]]) * g[b][sm[b]];
+            if (a == b) {
+                tp = piso[sp[b]] + tp;
+                tm = piso[sm[b]] + tm;
+            }
+            d[b] = (tp - tm) * 0.5;
+        }
+        F[a] = -((d[0] + d[1]) + d[2]);
+    }
+}
+
 /* Collision of one streamed site (f_s, g_s hold the 19 pulled values).
  * physics 0: reference collision (kernels.py:96-125 op order).
- * physics 1: Guo-forced f with F = -phi grad(mu); g_eq with the lam*(gamma mu - phi cs2) term.
+ * physics 1: Guo-forced f with F = -phi grad(mu) (a, b, c = grad mu); g_eq with
+ *            the lam*(gamma mu - phi cs2) term.
+ * physics 2: as 1 with the force given directly (a, b, c = F, stress_force).
  * Returns 0, or 1 if rho <= 0 (site left as streamed). */
 static int collide_site(double *fs, double *gs, double mu, double gmx, double gmy,
                         double gmz, const orc_fluid_params *p)
@@ -226,10 +292,16 @@ static int collide_site(double *fs, double *gs, double mu, double gmx, double gm
 
     const double cs2 = p->cs2;
     double Fx = 0.0, Fy = 0.0, Fz = 0.0, ux, uy, uz;
-    if (p->physics == 1) {
-        Fx = -(phi * gmx);
-        Fy = -(phi * gmy);
-        Fz = -(phi * gmz);
+    if (p->physics >= 1) {
+        if (p->physics == 1) {
+            Fx = -(phi * gmx);
+            Fy = -(phi * gmy);
+            Fz = -(phi * gmz);
+        } else {
+            Fx = gmx;
+            Fy = gmy;
+            Fz = gmz;
+        }
         ux = (jx + 0.5 * Fx) / rho;
         uy = (jy + 0.5 * Fy) / rho;
         uz = (jz + 0.5 * Fz) / rho;
@@ -250,7 +322,7 @@ static int collide_site(double *fs, double *gs, double mu, double gmx, double gm
         double feq = p->wv[i] * rho * bracket;
         double geq = p->wv[i] * phi * bracket;
         double fn = fs[i] - (fs[i] - feq) / p->tau_f;
-        if (p->physics == 1) {
+        if (p->physics >= 1) {
             double cF = (cx * Fx + cy * Fy) + cz * Fz;
             double src = (srcpre * p->wv[i]) * ((cF - uF) / cs2 + (udotc * cF) / (cs2 * cs2));
             fn = fn + src;
@@ -275,10 +347,20 @@ int64_t orc_fluid_step(const double *f_in, const double *g_in, double *f_out,
     orc_stream(f_in, f_out, Q, padded, nx, ny, nz);
     orc_stream(g_in, g_out, Q, padded, nx, ny, nz);
     orc_phi(g_out, phi, padded, nsites);
-    if (p->physics == 1)
+    if (p->physics >= 1)
         orc_mu(phi, mu, nx, ny, nz, p->A, p->B, p->kappa);
     else
         memset(mu, 0, sizeof(double) * nsites);
+    double *aux = NULL, *gr[3] = {NULL, NULL, NULL};
+    if (p->physics == 2) {
+        aux = (double *)malloc(sizeof(double) * 4 * (size_t)nsites);
+        if (!aux) return -2;
+        gr[0] = aux + nsites;
+        gr[1] = aux + 2 * nsites;
+        gr[2] = aux + 3 * nsites;
+        orc_stress(phi, mu, aux, gr[0], gr[1], gr[2], nx, ny, nz, p->A, p->B, p->kappa);
+    }
+    const double *const grc[3] = {gr[0], gr[1], gr[2]};
     int64_t bad = -1;
 #pragma omp parallel for schedule(static) reduction(max : bad)
     for (int64_t x = 0; x < nx; ++x) {
@@ -287,7 +369,13 @@ int64_t orc_fluid_step(const double *f_in, const double *g_in, double *f_out,
             for (int64_t z = 0; z < nz; ++z) {
                 int64_t s = site_of(x, y, z, ny, nz);
                 double gmx = 0.0, gmy = 0.0, gmz = 0.0, m = mu[s];
-                if (p->physics == 1) {
+                if (p->physics == 2) {
+                    double F[3];
+                    stress_force(aux, grc, p->kappa, x, y, z, nx, ny, nz, F);
+                    gmx = F[0];
+                    gmy = F[1];
+                    gmz = F[2];
+                } else if (p->physics == 1) {
                     gmx = (mu[site_of(wrap(x + 1, nx), y, z, ny, nz)] -
                            mu[site_of(wrap(x - 1, nx), y, z, ny, nz)]) * 0.5;
                     gmy = (mu[site_of(x, wrap(y + 1, ny), z, ny, nz)] -
@@ -309,5 +397,6 @@ int64_t orc_fluid_step(const double *f_in, const double *g_in, double *f_out,
                 }
             }
     }
+    free(aux);
     return bad;
 }
