@@ -78,6 +78,9 @@ def parse_args(argv=None):
                    help="exact: bitwise equal to the reference arithmetic (default); fast: "
                         "FMA/reciprocal arithmetic within 1e-12")
     p.add_argument("--vvl", type=int, default=1)
+    p.add_argument("--physics", choices=("binary", "binary-stress", "passive"), default="binary",
+                   help="force form: -phi grad mu (default, north star), the momentum-conserving "
+                        "stress divergence, or none")
     p.add_argument("--tau", type=float, default=1.0,
                    help="tau_f = tau_g (reference default 1.0, model.py:48-49)")
     p.add_argument("--e2e-steps", type=int, default=48,
@@ -323,7 +326,7 @@ def run_ours(args, rank, world, local):
     shape = lk.LatticeShape(nx, ny, nzl * world)
     mode = lk.MODE_FAST if args.mode == "fast" else lk.MODE_EXACT
     model = lk.D3Q19Model(tau_f=args.tau, tau_g=args.tau)
-    sim = lk.BinaryFluid(shape, model=model, physics="binary", mode=mode, vvl=args.vvl,
+    sim = lk.BinaryFluid(shape, model=model, physics=args.physics, mode=mode, vvl=args.vvl,
                          rank=rank, nranks=world, device=local, use_graph=False)
     fused = args.fuse
     sim.set_fuse(fused, args.fuse_lag)
@@ -425,7 +428,9 @@ def run_ours(args, rank, world, local):
                        "lattice": f"{nx}x{ny}x{nzl * world}",
                        "shape_per_gpu": f"{nx}x{ny}x{nzl}",
                        "mode": args.mode, "vvl": args.vvl, "tau": args.tau,
-                       "physics": "binary free energy",
+                       "physics": {"binary": "binary free energy, F = -phi grad mu",
+                                   "binary-stress": "binary free energy, F = -div P",
+                                   "passive": "passive (reference collision)"}[args.physics],
                        "fused": fused, "fuse_lag": args.fuse_lag if fused else None,
                        "l2": f"state {4 * 19 * 8 * nx * ny * nzl / 1e9:.1f} GB/GPU >> 126 MB L2, "
                              "no flush needed",

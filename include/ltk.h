@@ -162,7 +162,9 @@ typedef struct {
     double lam[LTK_Q];  /* g_eq chemical-potential weights */
     double cs2, tau_f, tau_g;
     double A, B, kappa, gamma; /* mu = A phi + B phi^3 - kappa lap(phi); mobility gamma */
-    int32_t physics;    /* 0 = passive (reference collision), 1 = free-energy binary fluid */
+    int32_t physics;    /* 0 = passive (reference collision), 1 = free-energy binary fluid
+                         * with F = -phi grad(mu), 2 = same with the momentum-conserving
+                         * F = -div P (chemical pressure tensor; engine only) */
     int32_t mode;       /* ltk_mode */
 } ltk_fluid_params;
 

@@ -177,10 +177,13 @@ static void launch_cs_exact(const FluidArgs &a, int vvl, cudaStream_t st) {
 
 static int launch_cs(const FluidArgs &a, int vvl, int mode, int phys, cudaStream_t st) {
     if (a.nthreads <= 0) return LTK_OK;
-    if (use_cs_tma(a, vvl)) return launch_cs_tma(a, mode, phys, st);
+    if (phys != 2 && use_cs_tma(a, vvl)) return launch_cs_tma(a, mode, phys, st);
     if (vvl > 2) return fail(LTK_ERR_PLAN, "collide-stream supports vvl 1, 2 (got %d)", vvl);
-    if (mode == LTK_MODE_EXACT && phys == 1) launch_cs_exact<1>(a, vvl, st);
+    if (phys == 2 && !a.aux) return fail(LTK_ERR_CONFIG, "stress form needs the engine's aux arrays");
+    if (mode == LTK_MODE_EXACT && phys == 2) launch_cs_exact<2>(a, vvl, st);
+    else if (mode == LTK_MODE_EXACT && phys == 1) launch_cs_exact<1>(a, vvl, st);
     else if (mode == LTK_MODE_EXACT) launch_cs_exact<0>(a, vvl, st);
+    else if (phys == 2) launch_cs_t<LTK_MODE_FAST, 2, 0>(a, vvl, st);
     else if (phys == 1) launch_cs_t<LTK_MODE_FAST, 1, 0>(a, vvl, st);
     else launch_cs_t<LTK_MODE_FAST, 0, 0>(a, vvl, st);
     LTK_CHECK_LAUNCH("k_collide_stream");
@@ -484,12 +487,15 @@ static FluidArgs engine_args(const ltk_fluid *e, int in_state) {
     a.phi_next = e->phi_of(1 - in_state);
     a.mu = e->mu;
     a.mu_out = e->mu;
+    a.astride = e->phi_stride;
+    a.aux = e->prm.physics == 2 ? e->mu + e->phi_stride : nullptr;  // after mu, same allocation
     a.err = singular_word();
     if (e->transport == kLocal) {  // periodic images into this slab
         a.img_f_up = a.img_f_dn = a.f_out;
         a.img_g_up = a.img_g_dn = a.g_out;
         a.img_phi_up = a.img_phi_dn = e->phi_of(in_state);
         a.img_mu_up = a.img_mu_dn = e->mu;
+        a.img_aux_up = a.img_aux_dn = a.aux;
     } else if (e->transport == kPeer) {  // images into the neighbours over NVLink
         a.img_f_up = e->up.fg[1 - in_state][0];
         a.img_g_up = e->up.fg[1 - in_state][1];
@@ -499,6 +505,10 @@ static FluidArgs engine_args(const ltk_fluid *e, int in_state) {
         a.img_phi_dn = e->dn.phi[in_state];
         a.img_mu_up = e->up.mu;
         a.img_mu_dn = e->dn.mu;
+        if (a.aux) {  // peers share the layout: their aux follows their mu
+            a.img_aux_up = e->up.mu + e->phi_stride;
+            a.img_aux_dn = e->dn.mu + e->phi_stride;
+        }
     }
     return a;
 }
@@ -533,11 +543,18 @@ static int exchange(ltk_fluid *e, int kind, int s) {
                 LTK_NCCL(n.Recv(plane(e->fg[s][d], sl, kDown[j], halo_hi), PL, ncclFloat64, up,
                                 e->comm, e->comm_st));
     } else {
-        double *b = kind == 1 ? e->phi_of(s) : e->mu;
-        LTK_NCCL(n.Send(b + top * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
-        LTK_NCCL(n.Send(b + bot * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
-        LTK_NCCL(n.Recv(b + halo_lo * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
-        LTK_NCCL(n.Recv(b + halo_hi * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
+        // kind 1: phi; kind 2: mu, and for the stress form the 4 aux arrays after it
+        const int nb = (kind == 2 && e->prm.physics == 2) ? 5 : 1;
+        for (int k = 0; k < nb; ++k) {
+            double *b = (kind == 1 ? e->phi_of(s) : e->mu) + (long long)k * e->phi_stride;
+            LTK_NCCL(n.Send(b + top * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
+            LTK_NCCL(n.Send(b + bot * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
+        }
+        for (int k = 0; k < nb; ++k) {
+            double *b = (kind == 1 ? e->phi_of(s) : e->mu) + (long long)k * e->phi_stride;
+            LTK_NCCL(n.Recv(b + halo_lo * PL, PL, ncclFloat64, down, e->comm, e->comm_st));
+            LTK_NCCL(n.Recv(b + halo_hi * PL, PL, ncclFloat64, up, e->comm, e->comm_st));
+        }
     }
     LTK_NCCL(n.GroupEnd());
     return LTK_OK;
@@ -577,7 +594,7 @@ static int cs_planes(ltk_fluid *e, FluidArgs &a, long long lo, long long hi, cud
     const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
     if (hi <= lo) return LTK_OK;
     set_planes(a, vvl, lo, hi);
-    if (e->fuse && a.ny * (a.nx / vvl) >= kTPB &&
+    if (e->fuse && e->prm.physics != 2 && a.ny * (a.nx / vvl) >= kTPB &&
         fuse_fields(a, vvl, (int)lo + 1, (int)hi - 1, e->fuse_lag, e->fsync)) {
         if (a.ncta != e->fuse_ncta) {  // launch epochs are ticket / ncta: restart the count
             LTK_CUDA(cudaMemsetAsync(e->fsync, 0, (size_t)(e->nzl + 1) * 8, st));
@@ -606,7 +623,7 @@ static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof, int nxt
         // interior planes came with the previous step's collide-stream
         LTK_RC(phi_rest(e, a, 0, nzl, phi));
         if (prof) cudaEventRecord(e->pev[1], st);
-        if (phys == 1) {
+        if (phys >= 1) {
             set_planes(a, vvl, 0, nzl);
             LTK_RC(launch_mu(a, vvl, st));
         }
@@ -635,7 +652,7 @@ static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof, int nxt
     LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[0], 0));
     LTK_RC(boundary(phi));
     if (prof) cudaEventRecord(e->pev[1], st);
-    if (phys == 1) {
+    if (phys >= 1) {
         // (2) phi faces || mu interior
         LTK_CUDA(cudaEventRecord(e->ev_fork[1], st));
         LTK_CUDA(cudaStreamWaitEvent(e->comm_st, e->ev_fork[1], 0));
@@ -655,7 +672,7 @@ static int enqueue_step(ltk_fluid *e, int s, cudaStream_t st, bool prof, int nxt
     }
     if (prof) cudaEventRecord(e->pev[2], st);
     LTK_RC(cs_planes(e, a, in_lo, in_hi, st, nxt));
-    if (phys == 1) LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[2], 0));
+    if (phys >= 1) LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[2], 0));
     LTK_RC(boundary([&] { return launch_cs(a, vvl, mode, phys, st); }));
     if (prof) cudaEventRecord(e->pev[3], st);
     return LTK_OK;
@@ -768,7 +785,7 @@ static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof, in
     LTK_RC(boundary(phi));
     LTK_RC(peer_signal(e, t4 + 2, st));
     if (prof) cudaEventRecord(e->pev[1], st);
-    if (phys == 1) {
+    if (phys >= 1) {
         LTK_RC(ranges(1, nzl - 1, mu));
         LTK_RC(peer_wait(e, t4 + 2, st));  // phi halos
         LTK_RC(boundary(mu));
@@ -857,6 +874,14 @@ static int preload_step_kernels() {
     preload_cs<LTK_MODE_EXACT, 1>(fa);
     preload_cs<LTK_MODE_FAST, 0>(fa);
     preload_cs<LTK_MODE_FAST, 1>(fa);
+    // stress form: register collide-stream only (no fused / TMA variants)
+    cudaFuncGetAttributes(&fa, k_collide_stream<1, LTK_MODE_FAST, 2, 0>);
+    cudaFuncGetAttributes(&fa, k_collide_stream<2, LTK_MODE_FAST, 2, 0>);
+    for (auto k : {k_collide_stream<1, LTK_MODE_EXACT, 2, 0>, k_collide_stream<1, LTK_MODE_EXACT, 2, 1>,
+                   k_collide_stream<1, LTK_MODE_EXACT, 2, 2>, k_collide_stream<1, LTK_MODE_EXACT, 2, 3>,
+                   k_collide_stream<2, LTK_MODE_EXACT, 2, 0>, k_collide_stream<2, LTK_MODE_EXACT, 2, 1>,
+                   k_collide_stream<2, LTK_MODE_EXACT, 2, 2>, k_collide_stream<2, LTK_MODE_EXACT, 2, 3>})
+        cudaFuncGetAttributes(&fa, k);
     LTK_CUDA(cudaFuncSetAttribute(k_mu_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)(200 * 1024)));
     LTK_CUDA(cudaFuncSetAttribute(k_mu_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1032,7 +1057,7 @@ int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank, in
     if (p->tau_f <= 0.5 || p->tau_g <= 0.5) return fail(LTK_ERR_CONFIG, "tau must be > 0.5");
     if (p->mode != LTK_MODE_EXACT && p->mode != LTK_MODE_FAST)
         return fail(LTK_ERR_CONFIG, "unknown mode %d", p->mode);
-    if (p->physics != 0 && p->physics != 1) return fail(LTK_ERR_CONFIG, "unknown physics");
+    if (p->physics < 0 || p->physics > 2) return fail(LTK_ERR_CONFIG, "unknown physics");
     ltk_fluid *e = new (std::nothrow) ltk_fluid();
     if (!e) return fail(LTK_ERR_ALLOC, "host allocation failed");
     e->nx = nx;
@@ -1082,7 +1107,9 @@ int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank, in
     e->fsync = (unsigned long long *)ptr;
     if (const char *v = getenv("LTK_FUSE")) e->fuse = atoi(v) != 0;  // default off
     if (const char *v = getenv("LTK_FUSE_LAG")) e->fuse_lag = std::max(0, atoi(v));
-    if ((rc = ltk_malloc(&ptr, plane_bytes))) {
+    // mu followed by the stress form's 4 aux arrays (p_iso, grad phi), one
+    // allocation so one IPC handle maps all of them
+    if ((rc = ltk_malloc(&ptr, 5 * (size_t)e->phi_stride * sizeof(double)))) {
         ltk_fluid_destroy(e);
         return rc;
     }
@@ -1162,6 +1189,9 @@ int ltk_fluid_stream(const ltk_fluid *e, void **stream) {
 
 int ltk_fluid_set_params(ltk_fluid *e, const ltk_fluid_params *p) {
     if (p->tau_f <= 0.5 || p->tau_g <= 0.5) return fail(LTK_ERR_CONFIG, "tau must be > 0.5");
+    if (p->mode != LTK_MODE_EXACT && p->mode != LTK_MODE_FAST)
+        return fail(LTK_ERR_CONFIG, "unknown mode %d", p->mode);
+    if (p->physics < 0 || p->physics > 2) return fail(LTK_ERR_CONFIG, "unknown physics");
     e->prm = *p;
     drop_graphs(e);
     return LTK_OK;

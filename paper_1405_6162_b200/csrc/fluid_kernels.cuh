@@ -37,6 +37,10 @@ struct FluidArgs {
     double *phi_out;
     double *mu_out;
     double *phi_next;  // k_cs_phi: phi of the state being written
+    // physics 2 (stress form): p_iso, d_x phi, d_y phi, d_z phi, slab layout like
+    // mu, at aux + k * astride; written by the mu kernels, read by collide-stream
+    double *aux, *img_aux_up, *img_aux_dn;
+    long long astride;
     long long *err;
     int nx, ny, nzl, z_lo, nplanes;
     // halo image targets (nullptr = none): buffers of the slab above (up) /
@@ -149,6 +153,35 @@ __global__ void __launch_bounds__(256) k_phi(const FluidArgs a) {
 }
 
 // ------------------------------------------------------------------ mu
+// physics 2 side outputs of the mu kernels at storage offset o = zs*PL + off:
+// p_iso and the central gradient of phi (oracle orc_stress op order), plus
+// their halo images for the boundary planes (like mu's).
+__device__ __forceinline__ void stress_store(const FluidArgs &a, int z, long long off, double ph,
+                                             double mu, double xp, double xm, double yp, double ym,
+                                             double zp, double zm) {
+    using M = Exact;
+    const double gx = M::mul(M::sub(xp, xm), 0.5);
+    const double gy = M::mul(M::sub(yp, ym), 0.5);
+    const double gz = M::mul(M::sub(zp, zm), 0.5);
+    const double gsq = M::add(M::add(M::mul(gx, gx), M::mul(gy, gy)), M::mul(gz, gz));
+    const double pp = M::mul(ph, ph);
+    const double fb = M::add(M::mul(M::mul(0.5, a.A), pp), M::mul(M::mul(0.25, a.B), M::mul(pp, pp)));
+    const double piso = M::sub(M::sub(M::mul(ph, mu), fb), M::mul(M::mul(0.5, a.kappa), gsq));
+    const double v[4] = {piso, gx, gy, gz};
+    const long long o = (long long)(z + 1) * a.PL + off;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a.aux[k * a.astride + o] = v[k];
+    if (z == 0 && a.img_aux_dn) {
+        const long long h = (long long)(a.nzl + 1) * a.PL + off;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a.img_aux_dn[k * a.astride + h] = v[k];
+    }
+    if (z == a.nzl - 1 && a.img_aux_up) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a.img_aux_up[k * a.astride + off] = v[k];
+    }
+}
+
 // mu = (A phi + B phi^3) - kappa lap, lap = (((((phi(x+1) + phi(x-1)) + phi(y+1))
 //      + phi(y-1)) + phi(z+1)) + phi(z-1)) - 6 phi   (oracle orc_mu op order)
 template <int VVL>
@@ -173,6 +206,12 @@ __global__ void __launch_bounds__(256) k_mu(const FluidArgs a) {
         const double p3 = __dmul_rn(__dmul_rn(ph, ph), ph);
         mu[k] = __dsub_rn(__dadd_rn(__dmul_rn(a.A, ph), __dmul_rn(a.B, p3)),
                           __dmul_rn(a.kappa, lap));
+        if (a.aux)
+            stress_store(a, p.z, (long long)p.y * a.nx + x, ph, mu[k],
+                         __ldg(c + (long long)p.y * a.nx + xp), __ldg(c + (long long)p.y * a.nx + xm),
+                         __ldg(c + (long long)yp * a.nx + x), __ldg(c + (long long)ym * a.nx + x),
+                         __ldg(c + a.PL + (long long)p.y * a.nx + x),
+                         __ldg(c - a.PL + (long long)p.y * a.nx + x));
     }
     const long long off = (long long)p.y * a.nx + p.x0;
     store_vec<VVL>(a.mu_out + (long long)(p.z + 1) * a.PL + off, mu);
@@ -211,10 +250,16 @@ __device__ __forceinline__ void fsite_finish(FSite &s, double gmx, double gmy, d
                                              const FluidArgs &a) {
     using M = Exact;
     if constexpr (MODE == LTK_MODE_EXACT) {
-        if constexpr (PHYS == 1) {
-            s.Fx = -M::mul(s.phi, gmx);
-            s.Fy = -M::mul(s.phi, gmy);
-            s.Fz = -M::mul(s.phi, gmz);
+        if constexpr (PHYS >= 1) {
+            if constexpr (PHYS == 1) {
+                s.Fx = -M::mul(s.phi, gmx);
+                s.Fy = -M::mul(s.phi, gmy);
+                s.Fz = -M::mul(s.phi, gmz);
+            } else {  // the stress-divergence force itself
+                s.Fx = gmx;
+                s.Fy = gmy;
+                s.Fz = gmz;
+            }
             const double rr = __drcp_rn(s.rho);  // RN(1/rho): three divisions by rho
             s.ux = div_rcp(M::add(s.jx, M::mul(0.5, s.Fx)), s.rho, rr);
             s.uy = div_rcp(M::add(s.jy, M::mul(0.5, s.Fy)), s.rho, rr);
@@ -232,10 +277,16 @@ __device__ __forceinline__ void fsite_finish(FSite &s, double gmx, double gmy, d
         s.t = div_rcp(usq, a.c1, a.a3);
     } else {
         const double inv = 1.0 / s.rho;
-        if constexpr (PHYS == 1) {
-            s.Fx = -(s.phi * gmx);
-            s.Fy = -(s.phi * gmy);
-            s.Fz = -(s.phi * gmz);
+        if constexpr (PHYS >= 1) {
+            if constexpr (PHYS == 1) {
+                s.Fx = -(s.phi * gmx);
+                s.Fy = -(s.phi * gmy);
+                s.Fz = -(s.phi * gmz);
+            } else {
+                s.Fx = gmx;
+                s.Fy = gmy;
+                s.Fz = gmz;
+            }
             s.ux = fma(0.5, s.Fx, s.jx) * inv;
             s.uy = fma(0.5, s.Fy, s.jy) * inv;
             s.uz = fma(0.5, s.Fz, s.jz) * inv;
@@ -267,7 +318,7 @@ __device__ __forceinline__ void frelax(double &f, double &g, double q, double sq
         double fn;
         if constexpr (T1 & 1) fn = M::sub(f, df);
         else fn = M::sub(f, div_rcp(df, a.tau_f, a.inv_tau_f));
-        if constexpr (PHYS == 1) {
+        if constexpr (PHYS >= 1) {
             const double ud = dot_c<cx(I), cy(I), cz(I), M>(s.ux, s.uy, s.uz);
             const double cF = dot_c<cx(I), cy(I), cz(I), M>(s.Fx, s.Fy, s.Fz);
             const double src =
@@ -287,7 +338,7 @@ __device__ __forceinline__ void frelax(double &f, double &g, double q, double sq
         const double feq = (a.wv[I] * s.rho) * br;
         double geq = (a.wv[I] * s.phi) * br;
         double fn = fma(feq - f, a.inv_tau_f, f);
-        if constexpr (PHYS == 1) {
+        if constexpr (PHYS >= 1) {
             const double cF = dot_c<cx(I), cy(I), cz(I), Fast>(s.Fx, s.Fy, s.Fz);
             const double src = (a.srcpre * a.wv[I]) *
                                fma(ud * cF, a.inv_cs2sq, (cF - s.uF) * a.inv_cs2);
@@ -349,6 +400,52 @@ struct MuGlobal {
     }
 };
 
+// physics 2: mu(x) and the stress-divergence force at lane k (oracle
+// stress_force op order): F_a = -((D_x P_ax + D_y P_ay) + D_z P_az),
+// D_b h = (h(+b) - h(-b)) * 0.5, P_aa = p_iso + ((kappa g_a) g_a),
+// P_ab = (kappa g_a) g_b, from the aux arrays the mu kernel wrote.
+template <int VVL>
+struct StressGlobal {
+    const FluidArgs &a;
+    const Pos &p;
+    __device__ __forceinline__ void operator()(int k, double &mu, double &Fx, double &Fy,
+                                               double &Fz) const {
+        using M = Exact;
+        const long long PL = a.PL, as = a.astride;
+        const long long c = (long long)(p.z + 1) * PL + (long long)p.y * a.nx + (p.x0 + k);
+        const int x = p.x0 + k;
+        // neighbour offsets from the centre: +-x (periodic), +-y (periodic), +-z (halo planes)
+        const long long r = (long long)(p.z + 1) * PL + (long long)p.y * a.nx;
+        const long long sp[3] = {r + wrapi(x + 1, a.nx),
+                                 (long long)(p.z + 1) * PL + (long long)wrapi(p.y + 1, a.ny) * a.nx + x,
+                                 c + PL};
+        const long long sm[3] = {r + wrapi(x - 1, a.nx),
+                                 (long long)(p.z + 1) * PL + (long long)wrapi(p.y - 1, a.ny) * a.nx + x,
+                                 c - PL};
+        mu = __ldg(a.mu + c);
+        const double *piso = a.aux, *g[3] = {a.aux + as, a.aux + 2 * as, a.aux + 3 * as};
+        double F[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double dd[3];
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                double tp = M::mul(M::mul(a.kappa, __ldg(g[d] + sp[b])), __ldg(g[b] + sp[b]));
+                double tm = M::mul(M::mul(a.kappa, __ldg(g[d] + sm[b])), __ldg(g[b] + sm[b]));
+                if (d == b) {
+                    tp = M::add(__ldg(piso + sp[b]), tp);
+                    tm = M::add(__ldg(piso + sm[b]), tm);
+                }
+                dd[b] = M::mul(M::sub(tp, tm), 0.5);
+            }
+            F[d] = -M::add(M::add(dd[0], dd[1]), dd[2]);
+        }
+        Fx = F[0];
+        Fy = F[1];
+        Fz = F[2];
+    }
+};
+
 template <int VVL, int MODE, int PHYS, int T1, int HINT, class MuFn>
 __device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, double (&F)[Q][VVL],
                                           double (&G)[Q][VVL], const MuFn &mufn) {
@@ -373,7 +470,7 @@ __device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, doub
 #pragma unroll
         for (int i = 0; i < Q; ++i) st[k].phi = M::add(st[k].phi, G[i][k]);
         double gmx = 0.0, gmy = 0.0, gmz = 0.0;
-        if constexpr (PHYS == 1) mufn(k, st[k].mu, gmx, gmy, gmz);
+        if constexpr (PHYS >= 1) mufn(k, st[k].mu, gmx, gmy, gmz);
         ok[k] = !(st[k].rho <= 0.0);
         if (ok[k]) {
             fsite_finish<MODE, PHYS>(st[k], gmx, gmy, gmz, a);
@@ -423,7 +520,8 @@ template <int VVL, int MODE, int PHYS, int T1, int HINT>
 __device__ __forceinline__ void cs_site(const FluidArgs &a, const Pos &p) {
     double F[Q][VVL], G[Q][VVL];
     cs_load<VVL, HINT>(a, p, F, G);
-    cs_finish<VVL, MODE, PHYS, T1, HINT>(a, p, F, G, MuGlobal<VVL>{a, p});
+    if constexpr (PHYS == 2) cs_finish<VVL, MODE, PHYS, T1, HINT>(a, p, F, G, StressGlobal<VVL>{a, p});
+    else cs_finish<VVL, MODE, PHYS, T1, HINT>(a, p, F, G, MuGlobal<VVL>{a, p});
 }
 
 template <int VVL, int MODE, int PHYS, int T1, int HINT = 0>

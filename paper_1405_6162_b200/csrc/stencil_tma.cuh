@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(256) k_mu_col(const FluidArgs a) {
                                     __dmul_rn(a.kappa, lap));
         const long long off = r0 + x;
         a.mu_out[(long long)(z + 1) * PL + off] = mu;
+        if (a.aux) stress_store(a, z, off, pc, mu, vxp, vxm, vyp, vym, pp, pm);
         bool img = false;
         if (z == 0 && a.img_mu_dn) {
             a.img_mu_dn[(long long)(a.nzl + 1) * PL + off] = mu;
@@ -210,7 +211,8 @@ inline size_t mu_tma_smem(const FluidArgs &a) {
 }
 
 inline bool mu_tma_ok(const FluidArgs &a) {
-    return a.ny % mu_tma_rows(a.nx) == 0 && a.nx % 2 == 0 && mu_tma_smem(a) <= 200 * 1024;
+    return !a.aux && a.ny % mu_tma_rows(a.nx) == 0 && a.nx % 2 == 0 &&
+           mu_tma_smem(a) <= 200 * 1024;  // (no stress outputs)
 }
 
 }  // namespace ltk

@@ -34,7 +34,11 @@ MODE_FAST = nat.MODE_FAST
 CS_REG = nat.CS_REG
 CS_TMA = nat.CS_TMA
 MU_AUTO, MU_TMA, MU_PLAIN = nat.MU_AUTO, nat.MU_TMA, nat.MU_PLAIN
-PHYSICS = {"passive": 0, "binary": 1}
+#: passive: the reference collision after streaming; binary: free-energy binary
+#: fluid with the force F = -phi grad(mu); binary-stress: the same fluid with the
+#: momentum-conserving F = -div P of the chemical pressure tensor (stable flat
+#: interfaces at Ludwig-scale constants where the potential form is not)
+PHYSICS = {"passive": 0, "binary": 1, "binary-stress": 2}
 
 
 @dataclass(frozen=True)

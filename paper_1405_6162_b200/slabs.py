@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native as nat
-from .errors import ShapeError, SingularStateError
+from .errors import ConfigError, ShapeError, SingularStateError
 from .lattice import Field, FieldDescriptor, LatticeShape, field_create
 from .model import CZ_DOWN, CZ_UP, Q
 
@@ -112,6 +112,9 @@ class VirtualSlabs:
 
     def __init__(self, shape: LatticeShape, nslabs: int, params: nat.FluidParams,
                  vvl: int = 1, device: int = 0) -> None:
+        if params.physics == 2:
+            raise ConfigError("VirtualSlabs drives the C-ABI kernels (phi, mu, collide-stream); "
+                              "the stress form (physics 2) runs through BinaryFluid only")
         self.shape, self.P, self.params, self.vvl = shape, nslabs, params, vvl
         nat.check(nat.lib.ltk_set_device(device))
         self.stream = nat.stream_create()

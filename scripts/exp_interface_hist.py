@@ -12,6 +12,7 @@ from paper_1405_6162_b200.lattice import FieldDescriptor, field_create  # noqa: 
 nx, ny, nz = (int(v) for v in sys.argv[1].split("x"))
 steps, every = int(sys.argv[2]), int(sys.argv[3])
 A, B, kappa, gamma, tau_f, tau_g = map(float, sys.argv[4:10])
+physics = sys.argv[10] if len(sys.argv) > 10 else "binary"
 fe = lk.FreeEnergy(A=A, B=B, kappa=kappa, gamma=gamma)
 model = lk.D3Q19Model(tau_f=tau_f, tau_g=tau_g)
 shape = lk.LatticeShape(nx, ny, nz)
@@ -27,7 +28,7 @@ for i in range(19):
 n, P = shape.nsites, desc.padded_sites
 cv = model.cvf
 hist = []
-with lk.BinaryFluid(shape, model=model, free_energy=fe, mode=lk.MODE_FAST) as sim:
+with lk.BinaryFluid(shape, model=model, free_energy=fe, mode=lk.MODE_FAST, physics=physics) as sim:
     sim.load(f, g)
     for t in range(0, steps + 1, every):
         if t:
@@ -39,5 +40,5 @@ with lk.BinaryFluid(shape, model=model, free_energy=fe, mode=lk.MODE_FAST) as si
         uz = (cv[:, 2][:, None] * F).sum(0) / rho
         phi = G.sum(0)
         hist.append([t, float(np.abs(uz).max()), float(phi.max()), float(rho.max() - rho.min())])
-print(json.dumps({"A": A, "B": B, "kappa": kappa, "gamma": gamma, "tau_f": tau_f, "tau_g": tau_g,
+print(json.dumps({"physics": physics, "A": A, "B": B, "kappa": kappa, "gamma": gamma, "tau_f": tau_f, "tau_g": tau_g,
                   "xi": xi, "hist": hist}))

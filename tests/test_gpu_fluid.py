@@ -262,6 +262,91 @@ class TestTmaCollideStream:
             lk.cs_variant(prev)
 
 
+class TestStressForm:
+    """physics "binary-stress": the force as the divergence of the chemical
+    pressure tensor (mu kernels also write p_iso and grad phi; collide-stream
+    differentiates them).  Bitwise vs the oracle in EXACT mode, and the long
+    flat-interface run the potential form fails."""
+
+    @pytest.mark.parametrize("shape", [(16, 12, 10), (32, 16, 6), (7, 6, 5), (64, 8, 9)])
+    @pytest.mark.parametrize("graph", [True, False])
+    def test_exact_bitwise(self, lk, shape, graph):
+        f0, g0 = _state(lk, shape, 23)
+        model = lk.D3Q19Model(tau_f=0.8, tau_g=1.1)
+        with lk.BinaryFluid(lk.LatticeShape(*shape), model=model, physics="binary-stress",
+                            use_graph=graph) as sim:
+            sim.load(f0, g0)
+            sim.run(4)
+            f1, g1 = sim.fields()
+        of, og, _, _ = _oracle(f0, g0, shape, 4, 2, 0.8, 1.1)
+        assert np.array_equal(f1.data.view(np.uint64), of.view(np.uint64))
+        assert np.array_equal(g1.data.view(np.uint64), og.view(np.uint64))
+
+    def test_fast_within_1e12_and_momentum(self, lk):
+        shape = (32, 32, 32)
+        f0, g0 = _state(lk, shape, 11)
+        with lk.BinaryFluid(lk.LatticeShape(*shape), mode=lk.MODE_FAST,
+                            physics="binary-stress") as sim:
+            sim.load(f0, g0)
+            t0 = sim.totals()
+            sim.run(10)
+            t1 = sim.totals()
+            f1, g1 = sim.fields()
+        of, og, _, _ = _oracle(f0, g0, shape, 10, 2)
+        for got, ref in ((f1.data, of), (g1.data, og)):
+            rel = np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300))
+            assert rel <= 1e-12, rel
+        assert np.allclose(t1[1:4], t0[1:4], rtol=0, atol=1e-11)   # momentum conserved
+
+    def test_nccl_self_exchange(self, lk):
+        if not lk.nccl_available():
+            pytest.skip("libnccl.so.2 not loadable")
+        shape = (16, 8, 8)
+        f0, g0 = _state(lk, shape, 13)
+        with lk.BinaryFluid(lk.LatticeShape(*shape), physics="binary-stress",
+                            use_graph=False) as sim:
+            sim.attach_nccl(lk.nccl_unique_id())
+            sim.load(f0, g0)
+            sim.run(3)
+            f1, g1 = sim.fields()
+        of, og, _, _ = _oracle(f0, g0, shape, 3, 2)
+        assert np.array_equal(f1.data, of) and np.array_equal(g1.data, og)
+
+    def test_flat_interface_long_run_stable(self, lk):
+        # Ludwig-scale constants: 6000 steps of a periodic double flat interface.
+        # The potential form runs away here (|u| ~ 0.1, interfaces dissolving);
+        # the stress form keeps the spurious velocity ~1e-4 and phi* = +-1.
+        from paper_1405_6162_b200.lattice import FieldDescriptor, field_create
+
+        fe = lk.FreeEnergy(A=-0.0625, B=0.0625, kappa=0.04)
+        model = lk.D3Q19Model()
+        nx, ny, nz = 8, 8, 64
+        shape = lk.LatticeShape(nx, ny, nz)
+        desc = FieldDescriptor.create(19, shape.nsites)
+        f, g = field_create(desc), field_create(desc)
+        xi = np.sqrt(-2 * fe.kappa / fe.A)
+        z = np.arange(nz)
+        prof = np.tanh((z - nz / 4 + 0.5) / xi) * np.tanh((3 * nz / 4 - 0.5 - z) / xi)
+        phi0 = np.broadcast_to(prof, (nx, ny, nz)).reshape(-1)
+        for i in range(19):
+            f.component(i)[:] = model.wv[i]
+            g.component(i)[:] = model.wv[i] * phi0
+        res = {}
+        for physics in ("binary", "binary-stress"):
+            with lk.BinaryFluid(shape, model=model, free_energy=fe, physics=physics,
+                                mode=lk.MODE_FAST) as sim:
+                sim.load(f, g)
+                sim.run(6000)
+                f1, g1 = sim.fields()
+            n, P = shape.nsites, desc.padded_sites
+            F1 = f1.data.reshape(19, P)[:, :n]
+            u = (model.cvf.T @ F1) / F1.sum(0)
+            res[physics] = (float(np.abs(u).max()),
+                            float(g1.data.reshape(19, P)[:, :n].sum(0).max()))
+        assert res["binary"][0] > 1e-2
+        assert res["binary-stress"][0] < 5e-4 and res["binary-stress"][1] > 0.99
+
+
 class TestSlabDecomposition:
     """P virtual slabs on one GPU, halos moved with the C-ABI face/plane calls."""
 

@@ -93,7 +93,7 @@ def _worker(rank, world, port, shape, steps, physics, q):
 # variant: "plain" (three-kernel step), "fused" (k_cs_phi on the interior planes
 # of every slab; needs nzl >= 5), "tma" (k_cs_tma; nx a multiple of 128)
 @pytest.mark.parametrize("nslabs", [2, 3, 4])
-@pytest.mark.parametrize("physics", ["binary", "passive"])
+@pytest.mark.parametrize("physics", ["binary", "passive", "binary-stress"])
 @pytest.mark.parametrize("nz,variant", [(12, "plain"), (24, "plain"), (24, "fused"), (24, "tma")])
 def test_engines_in_one_process_bitwise(nslabs, physics, nz, variant):
     import paper_1405_6162_b200 as lk
@@ -133,7 +133,8 @@ def test_engines_in_one_process_bitwise(nslabs, physics, nz, variant):
     nzl = nz // nslabs
     got = [np.concatenate([p[k].components()[:, :nx * ny * nzl].reshape(19, nx, ny, nzl)
                            for p in parts], axis=3) for k in (0, 1)]
-    prm = orc.fluid_params(tau_f=0.9, tau_g=1.1, physics=1 if physics == "binary" else 0)
+    prm = orc.fluid_params(tau_f=0.9, tau_g=1.1,
+                           physics={"passive": 0, "binary": 1, "binary-stress": 2}[physics])
     P = f0.descriptor.padded_sites
     of, og, _, _ = orc.fluid_step(f0.data, g0.data, shape, P, prm, steps=steps)
     ref = [a.reshape(19, P)[:, :nx * ny * nz].reshape(19, nx, ny, nz) for a in (of, og)]
