@@ -387,6 +387,17 @@ class TestFullSizeProperties:
             rel = np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300))
             assert rel <= 1e-12, rel
 
+    def test_256_plane_stress_form_exact_vs_oracle(self, lk):
+        # the stress form at the BASELINE plane size: two EXACT steps bitwise
+        shape = (256, 256, 32)
+        f0, g0 = _state(lk, shape, 77)
+        with lk.BinaryFluid(lk.LatticeShape(*shape), physics="binary-stress") as sim:
+            sim.load(f0, g0)
+            sim.run(2)
+            f1, g1 = sim.fields()
+        of, og, _, _ = _oracle(f0, g0, shape, 2, 2)
+        assert np.array_equal(f1.data, of) and np.array_equal(g1.data, og)
+
     def test_256cube_long_run_conservation(self, lk):
         # 200 FAST steps: total mass and total phi conserved to rounding
         shape = lk.LatticeShape(256, 256, 256)
