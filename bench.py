@@ -252,9 +252,11 @@ def cpu_oracle_rate(shape, steps, seed, threads=None):
     if threads is None:
         threads = os.cpu_count() or 1
     orc.set_threads(threads)
-    orc.fluid_step(f, g, shape, p, prm, steps=1)  # warm-up (page faults, thread pool)
+    stepper = orc.FluidStepper(shape, p, prm)   # buffers allocated and touched here
+    stepper.load(f, g)
+    stepper.run(1)                              # warm-up (thread pool, caches)
     t0 = time.perf_counter()
-    orc.fluid_step(f, g, shape, p, prm, steps=steps)
+    stepper.run(steps)
     dt = time.perf_counter() - t0
     return n * steps / dt / 1e6, threads, dt
 
@@ -275,10 +277,11 @@ def run_reference(args, rank, world):
     prm = orc.fluid_params(tau_f=1.0, tau_g=1.0, physics=1)
     threads = os.cpu_count() or 1
     orc.set_threads(threads)
-    for _ in range(max(1, args.warmup)):
-        f, g, _, _ = orc.fluid_step(f, g, sample, p, prm, steps=1)
+    stepper = orc.FluidStepper(sample, p, prm)  # allocation and first touch untimed
+    stepper.load(f, g)
+    stepper.run(max(1, args.warmup))
     t0 = time.perf_counter()
-    f, g, _, _ = orc.fluid_step(f, g, sample, p, prm, steps=steps)
+    stepper.run(steps)
     dt = time.perf_counter() - t0
     mlups = n * steps / dt / 1e6
     line = {

@@ -325,3 +325,17 @@ class TestStressForm:
         assert res[1][1] > 1e-2                      # the potential form runs away
         assert res[2][1] < 5e-4 and res[2][1] < 2 * res[2][0] + 1e-5
         assert res[2][2] > 0.99
+
+
+def test_fluid_stepper_equals_fluid_step():
+    # bench.py's CPU timing path (preallocated buffers) computes the same steps
+    shape = (6, 5, 4)
+    f, g, n, p = _state(shape, 3)
+    prm = orc.fluid_params(tau_f=0.9, tau_g=1.1, physics=1)
+    ref_f, ref_g, _, _ = orc.fluid_step(f, g, shape, p, prm, steps=3)
+    st = orc.FluidStepper(shape, p, prm)
+    st.load(f, g)
+    st.run(1)
+    st.run(2)
+    sf, sg = st.state()
+    assert np.array_equal(sf, ref_f) and np.array_equal(sg, ref_g)
