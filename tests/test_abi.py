@@ -67,3 +67,32 @@ def test_no_gpu_means_loud_failure():
         lk.TargetDevice()
     with pytest.raises(lk.ConfigError):
         lk.BinaryFluid(lk.LatticeShape(4, 4, 4))
+
+
+def test_plain_c_host_compiles_and_links(tmp_path):
+    # include/ltk.h is a C header: a C99 host (the paper's targetDP setting,
+    # INTEGRATION.md §2) compiles against it and links libltk.so
+    src = tmp_path / "host.c"
+    src.write_text(r"""
+#include <stdio.h>
+#include "ltk.h"
+int main(void) {
+    ltk_collision_params p = {{0}, 1.0 / 3.0, 1.0, 1.0, LTK_MODE_EXACT, 0};
+    ltk_fluid_params q;
+    int64_t site = -1;
+    int n = 0;
+    (void)p; (void)q; (void)site;
+    if (ltk_abi_version() != 1) return 1;
+    if (ltk_device_count(&n) != LTK_OK && n != 0) return 2;
+    printf("abi %d devices %d\n", ltk_abi_version(), n);
+    return 0;
+}
+""")
+    exe = tmp_path / "host"
+    lib_dir = os.path.dirname(LIB)
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    str(src), "-L", lib_dir, "-lltk", f"-Wl,-rpath,{lib_dir}", "-o", str(exe)],
+                   check=True, capture_output=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    assert out.stdout.startswith("abi 1")
