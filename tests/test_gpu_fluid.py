@@ -282,6 +282,16 @@ class TestStressForm:
         assert np.array_equal(f1.data.view(np.uint64), of.view(np.uint64))
         assert np.array_equal(g1.data.view(np.uint64), og.view(np.uint64))
 
+    def test_vvl2_exact_bitwise(self, lk):
+        shape = (16, 8, 8)
+        f0, g0 = _state(lk, shape, 5)
+        with lk.BinaryFluid(lk.LatticeShape(*shape), physics="binary-stress", vvl=2) as sim:
+            sim.load(f0, g0)
+            sim.run(3)
+            f1, g1 = sim.fields()
+        of, og, _, _ = _oracle(f0, g0, shape, 3, 2)
+        assert np.array_equal(f1.data, of) and np.array_equal(g1.data, og)
+
     def test_fast_within_1e12_and_momentum(self, lk):
         shape = (32, 32, 32)
         f0, g0 = _state(lk, shape, 11)

@@ -94,7 +94,8 @@ def _worker(rank, world, port, shape, steps, physics, q):
 # of every slab; needs nzl >= 5), "tma" (k_cs_tma; nx a multiple of 128)
 @pytest.mark.parametrize("nslabs", [2, 3, 4])
 @pytest.mark.parametrize("physics", ["binary", "passive", "binary-stress"])
-@pytest.mark.parametrize("nz,variant", [(12, "plain"), (24, "plain"), (24, "fused"), (24, "tma")])
+@pytest.mark.parametrize("nz,variant", [(12, "plain"), (24, "plain"), (24, "fused"), (24, "tma"),
+                                        (12, "vvl2")])
 def test_engines_in_one_process_bitwise(nslabs, physics, nz, variant):
     import paper_1405_6162_b200 as lk
     from oracle import oracle as orc
@@ -105,7 +106,8 @@ def test_engines_in_one_process_bitwise(nslabs, physics, nz, variant):
     model = lk.D3Q19Model(tau_f=0.9, tau_g=1.1)
     prev = lk.cs_variant(lk.CS_TMA if variant == "tma" else lk.CS_REG)
     sims = [lk.BinaryFluid(full, model=model, physics=physics, rank=r, nranks=nslabs,
-                           use_graph=False) for r in range(nslabs)]
+                           use_graph=False, vvl=2 if variant == "vvl2" else 1)
+            for r in range(nslabs)]
     for sim in sims:
         sim.set_fuse(variant == "fused", 1)
     try:
