@@ -432,6 +432,7 @@ struct ltk_fluid {
     unsigned long long *fsync = nullptr;
     unsigned fuse_ncta = 0;  // grid of the fused launches counted in fsync
     bool fuse = false;  // measured slower than the three-kernel step
+    bool peer_overlap = true;  // peer transport: boundary planes on comm_st (env LTK_PEER_OVERLAP)
     int fuse_lag = 1;
     int phi_lo = 0, phi_hi = 0;
     double *phi_of(int s) const { return phi + s * phi_stride; }
@@ -763,6 +764,12 @@ static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof, in
     const int vvl = e->vvl, mode = e->prm.mode, phys = e->prm.physics;
     const long long nzl = e->nzl;
     const unsigned long long t4 = 4ULL * (unsigned long long)e->step;
+    // Boundary planes on a second stream (bs): a phase's boundary planes need the
+    // neighbours' halos and the previous phase, never this phase's interior, so
+    // progress wait + boundary kernels (with their peer stores) + signal run
+    // concurrently with the interior kernel; the streams join before the next
+    // phase.  overlap off: everything in order on st.
+    cudaStream_t bs = e->peer_overlap ? e->comm_st : st;
     auto ranges = [&](long long lo, long long hi, auto launch_one) -> int {
         if (hi > lo) {
             set_planes(a, vvl, lo, hi);
@@ -775,27 +782,50 @@ static int enqueue_step_peer(ltk_fluid *e, int s, cudaStream_t st, bool prof, in
         if (nzl > 1) LTK_RC(ranges(nzl - 1, nzl, launch_one));
         return LTK_OK;
     };
-    auto phi = [&] { return launch_phi(a, vvl, st); };
-    auto mu = [&] { return launch_mu(a, vvl, st); };
-    auto cs = [&] { return launch_cs(a, vvl, mode, phys, st); };
+    auto fork = [&](int k) -> int {
+        if (bs == st) return LTK_OK;
+        LTK_CUDA(cudaEventRecord(e->ev_fork[k], st));
+        LTK_CUDA(cudaStreamWaitEvent(bs, e->ev_fork[k], 0));
+        return LTK_OK;
+    };
+    auto join = [&](int k) -> int {
+        if (bs == st) return LTK_OK;
+        LTK_CUDA(cudaEventRecord(e->ev_join[k], bs));
+        LTK_CUDA(cudaStreamWaitEvent(st, e->ev_join[k], 0));
+        return LTK_OK;
+    };
+    auto phi_a = [&] { return launch_phi(a, vvl, st); };
+    auto phi_b = [&] { return launch_phi(a, vvl, bs); };
+    auto mu_a = [&] { return launch_mu(a, vvl, st); };
+    auto mu_b = [&] { return launch_mu(a, vvl, bs); };
+    auto cs_b = [&] { return launch_cs(a, vvl, mode, phys, bs); };
     if (prof) cudaEventRecord(e->pev[0], st);
-    if (nzl > 2) LTK_RC(phi_rest(e, a, 1, nzl - 1, phi));
-    LTK_RC(peer_wait(e, t4 + (e->primed ? 1 : 0), st));  // f/g halos of state s
+    // phi: interior || (f/g halos of state s -> boundary planes -> signal 4t+2)
+    LTK_RC(fork(0));
+    LTK_RC(peer_wait(e, t4 + (e->primed ? 1 : 0), bs));
     e->primed = false;
-    LTK_RC(boundary(phi));
-    LTK_RC(peer_signal(e, t4 + 2, st));
+    LTK_RC(boundary(phi_b));
+    LTK_RC(peer_signal(e, t4 + 2, bs));
+    if (nzl > 2) LTK_RC(phi_rest(e, a, 1, nzl - 1, phi_a));
+    LTK_RC(join(0));
     if (prof) cudaEventRecord(e->pev[1], st);
+    // mu: interior || (phi halos -> boundary planes) ; signal 4t+3
+    LTK_RC(fork(1));
     if (phys >= 1) {
-        LTK_RC(ranges(1, nzl - 1, mu));
-        LTK_RC(peer_wait(e, t4 + 2, st));  // phi halos
-        LTK_RC(boundary(mu));
+        LTK_RC(peer_wait(e, t4 + 2, bs));
+        LTK_RC(boundary(mu_b));
     }
-    LTK_RC(peer_signal(e, t4 + 3, st));
+    LTK_RC(peer_signal(e, t4 + 3, bs));
+    if (phys >= 1) LTK_RC(ranges(1, nzl - 1, mu_a));
+    LTK_RC(join(1));
     if (prof) cudaEventRecord(e->pev[2], st);
+    // collide-stream: interior || (mu halos -> boundary planes -> signal 4t+4)
+    LTK_RC(fork(2));
+    LTK_RC(peer_wait(e, t4 + 3, bs));
+    LTK_RC(boundary(cs_b));
+    LTK_RC(peer_signal(e, t4 + 4, bs));
     LTK_RC(cs_planes(e, a, 1, nzl - 1, st, nxt));
-    LTK_RC(peer_wait(e, t4 + 3, st));  // mu halos
-    LTK_RC(boundary(cs));
-    LTK_RC(peer_signal(e, t4 + 4, st));
+    LTK_RC(join(2));
     if (prof) cudaEventRecord(e->pev[3], st);
     return LTK_OK;
 }
@@ -1106,6 +1136,7 @@ int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank, in
     }
     e->fsync = (unsigned long long *)ptr;
     if (const char *v = getenv("LTK_FUSE")) e->fuse = atoi(v) != 0;  // default off
+    if (const char *v = getenv("LTK_PEER_OVERLAP")) e->peer_overlap = atoi(v) != 0;
     if (const char *v = getenv("LTK_FUSE_LAG")) e->fuse_lag = std::max(0, atoi(v));
     // mu followed by the stress form's 4 aux arrays (p_iso, grad phi), one
     // allocation so one IPC handle maps all of them
