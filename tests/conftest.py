@@ -9,6 +9,10 @@ import sys
 
 import pytest
 
+# before any CUDA context: multi-engine peer tests use two streams per engine
+# (see paper_1405_6162_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
