@@ -339,3 +339,59 @@ def test_fluid_stepper_equals_fluid_step():
     st.run(2)
     sf, sg = st.state()
     assert np.array_equal(sf, ref_f) and np.array_equal(sg, ref_g)
+
+
+# ------------------------------------------------------------ properties (hypothesis)
+
+from hypothesis import given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+_dims = st.tuples(st.integers(1, 6), st.integers(1, 6), st.integers(1, 6))
+
+
+@settings(max_examples=25, deadline=None)
+@given(shape=_dims, seed=st.integers(0, 2 ** 31 - 1))
+def test_property_stream_c_equals_numpy_and_inverts(shape, seed):
+    n = shape[0] * shape[1] * shape[2]
+    p = -(-n // 16) * 16
+    rng = np.random.default_rng(seed)
+    f = np.zeros(19 * p)
+    f.reshape(19, p)[:, :n] = rng.random((19, n))
+    out = np.zeros_like(f)
+    orc.lib().orc_stream(orc._p(f), orc._p(out), 19, p, *shape)
+    assert np.array_equal(out, orc.stream_numpy(f, shape, p))
+    # pulling every component by -c_i undoes the stream
+    back = np.zeros_like(f)
+    o3 = out.reshape(19, p)[:, :n].reshape(19, *shape)
+    for i in range(19):
+        back.reshape(19, p)[i, :n] = np.roll(o3[i], tuple(-c for c in orc.CV[i]),
+                                             axis=(0, 1, 2)).ravel()
+    assert np.array_equal(back, f)
+
+
+@settings(max_examples=25, deadline=None)
+@given(shape=_dims, seed=st.integers(0, 2 ** 31 - 1))
+def test_property_stress_force_sums_to_zero(shape, seed):
+    # a discrete divergence telescopes on any periodic lattice
+    rng = np.random.default_rng(seed)
+    p3 = rng.uniform(-1, 1, shape)
+    prm = orc.fluid_params(physics=2)
+    mu3 = orc.mu_numpy(p3, [np.roll(p3, s, a) for a in range(3) for s in (-1, 1)], prm)
+    F = orc.stress_force_numpy(p3, mu3, prm)
+    scale = max(1.0, float(max(np.abs(f).max() for f in F)))
+    for comp in F:
+        assert abs(comp.sum()) <= 1e-13 * scale * comp.size
+
+
+@settings(max_examples=15, deadline=None)
+@given(shape=_dims, seed=st.integers(0, 2 ** 31 - 1), physics=st.sampled_from([0, 1, 2]),
+       tau_f=st.sampled_from([0.6, 1.0, 1.7]), tau_g=st.sampled_from([0.7, 1.0]))
+def test_property_c_and_numpy_full_step_bitwise(shape, seed, physics, tau_f, tau_g):
+    n = shape[0] * shape[1] * shape[2]
+    p = -(-n // 16) * 16
+    f, g = orc.random_binary_state(n, p, seed)
+    prm = orc.fluid_params(tau_f=tau_f, tau_g=tau_g, physics=physics)
+    fc, gc, _, _ = orc.fluid_step(f, g, shape, p, prm, steps=1)
+    fn, gn, _, _ = orc.fluid_step_numpy(f, g, shape, p, prm)
+    assert np.array_equal(fc.view(np.uint64), fn.view(np.uint64))
+    assert np.array_equal(gc.view(np.uint64), gn.view(np.uint64))
