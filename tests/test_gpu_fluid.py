@@ -509,3 +509,34 @@ class TestStencilKernels:
         finally:
             nat.free(d_phi)
             nat.free(d_mu)
+
+
+class TestRandomShapes:
+    """Hypothesis-driven parity: random lattice shapes (nx*ny even, the engine's
+    16-byte row rule), physics, tau and step counts, EXACT bitwise vs the oracle."""
+
+    def test_random_shapes_bitwise(self, lk):
+        from hypothesis import given, settings
+        from hypothesis import strategies as st
+
+        @settings(max_examples=30, deadline=None)
+        @given(nx=st.integers(1, 12), ny=st.integers(1, 12), nz=st.integers(1, 9),
+               physics=st.sampled_from(["passive", "binary", "binary-stress"]),
+               tau=st.sampled_from([(1.0, 1.0), (0.8, 1.3), (1.6, 0.7)]),
+               steps=st.integers(1, 3), seed=st.integers(0, 10 ** 6))
+        def check(nx, ny, nz, physics, tau, steps, seed):
+            if (nx * ny) % 2:
+                nx += 1
+            shape = (nx, ny, nz)
+            f0, g0 = _state(lk, shape, seed)
+            model = lk.D3Q19Model(tau_f=tau[0], tau_g=tau[1])
+            with lk.BinaryFluid(lk.LatticeShape(*shape), model=model, physics=physics) as sim:
+                sim.load(f0, g0)
+                sim.run(steps)
+                f1, g1 = sim.fields()
+            code = {"passive": 0, "binary": 1, "binary-stress": 2}[physics]
+            of, og, _, _ = _oracle(f0, g0, shape, steps, code, tau[0], tau[1])
+            assert np.array_equal(f1.data.view(np.uint64), of.view(np.uint64)), shape
+            assert np.array_equal(g1.data.view(np.uint64), og.view(np.uint64)), shape
+
+        check()
