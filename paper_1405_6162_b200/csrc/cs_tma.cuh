@@ -196,13 +196,13 @@ __global__ void __launch_bounds__(32 * ((NPW > 0 ? NPW : 1) + NCW), 1) k_cs_tma(
     // exceeds one tile may reach slot s while the slot's previous fill is still
     // in flight -- the parity of its phase would alias the phase before that.
     // Waiting for the tag first pins the barrier to this tile's phase.
-    __shared__ volatile long long slot_tile[STAGES];
+    __shared__ unsigned long long slot_tile[STAGES];  // accessed with shared-memory atomics
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], NPW > 0 ? 32 * NPW : 1);
             mbar_init(&empty[s], WPT);
-            slot_tile[s] = -1;
+            slot_tile[s] = ~0ull;
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -214,8 +214,14 @@ __global__ void __launch_bounds__(32 * ((NPW > 0 ? NPW : 1) + NCW), 1) k_cs_tma(
         long long k = 0;
         for (long long j = blockIdx.x; j < ntiles; j += G, ++k) {
             const int s = (int)(k % STAGES);
-            if (k >= STAGES) mbar_wait(&empty[s], (uint32_t)((k / STAGES - 1) & 1));
-            if (threadIdx.x == 0) slot_tile[s] = k;  // before the barrier is armed
+            if (k >= STAGES) {
+                mbar_wait(&empty[s], (uint32_t)((k / STAGES - 1) & 1));
+                // the consumers' generic-proxy reads of this slot happen before the
+                // async-proxy (TMA / cp.async) writes that refill it
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            if (threadIdx.x == 0)  // before the barrier is armed
+                atomicExch(&slot_tile[s], (unsigned long long)k);
             __syncwarp();
             double *sb = stage + (size_t)s * (Gm::stage_bytes / 8);
             if constexpr (NPW == 0) {
@@ -237,7 +243,8 @@ __global__ void __launch_bounds__(32 * ((NPW > 0 ? NPW : 1) + NCW), 1) k_cs_tma(
         const int xl = (int)(q % WPT) * 32 + lane;
         const long long j = blockIdx.x + k * G;
         const int s = (int)(k % STAGES);
-        while (slot_tile[s] != k) __nanosleep(32);  // the slot now receives tile k
+        while (atomicAdd(&slot_tile[s], 0ull) != (unsigned long long)k)  // slot receives tile k
+            __nanosleep(32);
         mbar_wait(&full[s], (uint32_t)((k / STAGES) & 1));
         const double *sb = stage + (size_t)s * (Gm::stage_bytes / 8);
         double F[Q][1], G_[Q][1];
