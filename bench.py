@@ -406,8 +406,8 @@ def run_ours(args, rank, world, local):
     # ---------------- CPU baseline (rank 0, N=1)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        # bounded sample, ~10 s of CPU work on a 16-thread host (~10 MLUPS)
-        sample, csteps = (nx, ny, min(64, nzl)), 24
+        # bounded sample, ~10 s of CPU work on the GPU box's 16 host threads (~20 MLUPS)
+        sample, csteps = (nx, ny, min(64, nzl)), 48
         rate, threads, dt = cpu_oracle_rate(sample, csteps, args.seed)
         cpu = {"value": rate, "unit": "MLUPS", "cores": threads, "kind": "port",
                "sample": f"{sample[0]}x{sample[1]}x{sample[2]} periodic lattice, {csteps} "
