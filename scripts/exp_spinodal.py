@@ -45,8 +45,12 @@ with lk.BinaryFluid(shape, model=model, free_energy=fe, physics=physics, mode=mo
         S = np.abs(np.fft.fftn(phi - phi.mean())) ** 2
         Sk = np.bincount(kbin.ravel(), S.ravel()) / np.maximum(np.bincount(kbin.ravel()), 1)
         kmax = int(np.argmax(Sk[1:N // 2]) + 1)
+        ks = np.arange(len(Sk))
+        tot = np.bincount(kbin.ravel(), S.ravel())
+        kmean = float((ks[1:N // 2] * tot[1:N // 2]).sum() / max(tot[1:N // 2].sum(), 1e-300))
         hist.append({"t": t, "mean_abs_phi": float(np.abs(phi).mean()), "free_energy": fen,
                      "max_u": float(np.abs(u).max()), "wavelength": N / kmax,
+                     "L": N / kmean if kmean > 0 else None,
                      "phi_sum": float(phi.sum()), "finite": bool(np.isfinite(F1).all())})
 print(json.dumps({"N": N, "physics": physics, "mode": "exact" if mode == lk.MODE_EXACT else "fast",
                   "hist": hist}))
