@@ -51,6 +51,18 @@ class TestCliOnDevice:
         assert any(l.startswith("PASS equivalence") for l in out.split("\n"))
         assert any(l.startswith("PASS conservation") for l in out.split("\n"))
 
+    @pytest.mark.parametrize("physics", ["binary", "binary-stress"])
+    def test_fluid_verify_passes(self, capsys, physics):
+        code = cli_main(["--verify", "--kernel", "binary-fluid", "--shape", "16x12x10",
+                         "--iters", "1", "--vvl", "1", "--physics", physics])
+        out = capsys.readouterr().out
+        assert code == 0, out
+        lines = [l for l in out.split("\n") if l.startswith(("PASS", "FAIL"))]
+        assert lines and all(l.startswith("PASS") for l in lines), lines
+        assert any("VVL 1 == VVL 2" in l for l in lines)
+        assert any("fixed point" in l for l in lines)
+        assert (physics == "binary-stress") == any("momentum" in l for l in lines)
+
     def test_fluid_and_stats(self, capsys, tmp_path):
         path = tmp_path / "o.csv"
         code = cli_main(["--kernel", "binary-fluid", "--shape", "16x16x16", "--vvl", "1,2",
