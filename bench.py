@@ -96,6 +96,10 @@ def parse_args(argv=None):
                         "three-kernel step")
     p.add_argument("--fuse-lag", type=int, default=1,
                    help="planes of slack between the collision and phi fronts of k_cs_phi")
+    p.add_argument("--layout", choices=("soa", "row"), default="row",
+                   help="f/g storage: component-major planes (soa) or row-blocked (row: "
+                        "the 19 components of an x-row adjacent); bitwise identical. "
+                        "The NCCL transport always uses soa")
     p.add_argument("--transport", choices=("peer", "nccl"), default="peer",
                    help="N>1 halo exchange: peer stores from the kernels (CUDA IPC over "
                         "NVLink) or NCCL send/recv")
@@ -333,6 +337,7 @@ def run_ours(args, rank, world, local):
                          rank=rank, nranks=world, device=local, use_graph=False)
     fused = args.fuse
     sim.set_fuse(fused, args.fuse_lag)
+    sim.set_layout(lk.LAYOUT_ROW if args.layout == "row" else lk.LAYOUT_SOA)
     if world > 1 and args.transport == "nccl":
         uid = lk.nccl_unique_id() if rank == 0 else None
         sim.attach_nccl(ctl.bcast_bytes(uid, 128))
@@ -340,6 +345,7 @@ def run_ours(args, rank, world, local):
         blobs = ctl.allgather_bytes(sim.ipc_blob())
         sim.attach_peers(blobs[(rank + 1) % world], blobs[(rank - 1) % world])
         ctl.barrier()  # every inbox reset before any neighbour primes it
+    layout = "row" if sim.set_layout(None) == lk.LAYOUT_ROW else "soa"
 
     # per-slab synthetic state in reference order (x*ny + y)*nzl + z
     slab_shape = lk.LatticeShape(nx, ny, nzl)
@@ -435,6 +441,7 @@ def run_ours(args, rank, world, local):
                                    "binary-stress": "binary free energy, F = -div P",
                                    "passive": "passive (reference collision)"}[args.physics],
                        "fused": fused, "fuse_lag": args.fuse_lag if fused else None,
+                       "layout": layout,
                        "l2": f"state {4 * 19 * 8 * nx * ny * nzl / 1e9:.1f} GB/GPU >> 126 MB L2, "
                              "no flush needed",
                        "parallelism": f"z-slab x{world}",

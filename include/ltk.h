@@ -265,6 +265,22 @@ int ltk_fluid_cs_variant(int32_t variant, int32_t *previous);
 #define LTK_MU_TMA 1
 #define LTK_MU_PLAIN 2
 int ltk_fluid_mu_variant(int32_t variant, int32_t *previous);
+
+/* f/g storage layout of an engine.  LTK_LAYOUT_SOA: component-major
+ * planes, element (i, zs, y, x) at i*cstride + zs*nx*ny + y*nx + x -- the
+ * ltk_slab layout every slab-level entry point above takes.  LTK_LAYOUT_ROW:
+ * row-blocked, element at zs*ny*19*nx + (y*19 + i)*nx + x (the 19 components
+ * of one x-row adjacent; even nx; the default of new engines with even nx,
+ * measured ~1.5% faster on the full step).  Results are bitwise identical; only the
+ * engine's own buffers change (ltk_fluid_buffers' f/g pointers then hold
+ * that layout).  Set before ltk_fluid_load and before attaching a transport
+ * (the state is undefined after a change); ltk_fluid_attach_nccl switches the
+ * slab to SoA (NCCL sends contiguous planes); peer slabs must agree.  The
+ * environment variable LTK_LAYOUT=0 makes SoA the default of new engines.  layout < 0 only queries (*previous).  Not in the reference: a
+ * B200 layout choice. */
+#define LTK_LAYOUT_SOA 0
+#define LTK_LAYOUT_ROW 1
+int ltk_fluid_set_layout(ltk_fluid *e, int32_t layout, int32_t *previous);
 /* Last step's per-kernel device times in ms (phi, mu, collide_stream, halo). */
 int ltk_fluid_profile(ltk_fluid *e, int32_t enable, float *ms4);
 

@@ -25,6 +25,7 @@ MODE_FAST = 1
 CS_REG = 0
 CS_TMA = 1
 MU_AUTO, MU_TMA, MU_PLAIN = 0, 1, 2
+LAYOUT_SOA, LAYOUT_ROW = 0, 1
 
 _ERRORS = {1: ConfigError, 2: BoundsError, 3: ShapeError, 4: AllocationError,
            5: LifecycleError, 6: PlanError, 7: DeviceError, 11: SingularStateError}
@@ -124,6 +125,7 @@ SIGNATURES = {
     "ltk_fluid_cs_variant": (ctypes.c_int, [_i32, ctypes.POINTER(_i32)]),
     "ltk_div_selftest": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
     "ltk_fluid_mu_variant": (ctypes.c_int, [_i32, ctypes.POINTER(_i32)]),
+    "ltk_fluid_set_layout": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(_i32)]),
     "ltk_fluid_profile": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(ctypes.c_float)]),
     "ltk_fluid_ipc_blob": (ctypes.c_int, [_vp, ctypes.c_char_p]),
     "ltk_fluid_attach_peers": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p]),

@@ -88,7 +88,7 @@ void preload_cs_tma(int nx) {
 }
 
 bool cs_tma_ok(const FluidArgs &a, int vvl) {
-    return vvl == 1 && a.nx % 128 == 0 && a.nthreads > 0;
+    return vvl == 1 && a.nx % 128 == 0 && a.nthreads > 0 && a.SI == a.cstride;  // SoA only
 }
 
 int launch_cs_tma(const FluidArgs &a, int mode, int phys, cudaStream_t st) {

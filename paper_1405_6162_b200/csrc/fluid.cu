@@ -45,6 +45,9 @@ static void fill_args(FluidArgs &a, const ltk_slab *s, const ltk_fluid_params *p
     a.nzl = (int)s->nzl;
     a.PL = s->nx * s->ny;
     a.cstride = s->cstride;
+    a.SI = s->cstride;  // SoA; the engine may switch to the row-blocked layout
+    a.SZ = a.PL;
+    a.SY = s->nx;
     a.nz_global = s->nzl;
     a.z0 = 0;
     if (p) {
@@ -260,21 +263,29 @@ static int launch_cs_phi(const FluidArgs &a, int vvl, int mode, int phys, cudaSt
 }
 
 // ------------------------------------------------------------------ plane copies
+// Each copy moves `rows` rows of `row` doubles (row even), rows `stride`
+// doubles apart on both sides; a contiguous plane is rows = 1, row = PL.
 struct PlaneCopies {
     const double *src[24];
     double *dst[24];
     int n;
-    long long PL;
+    long long PL;      // doubles per copy (rows * row)
+    long long row = 0; // 0: contiguous (row = PL)
+    long long stride = 0;
 };
 
 __global__ void __launch_bounds__(256) k_plane_copy(const PlaneCopies pc) {
     const int j = blockIdx.y;
-    const double2 *s = reinterpret_cast<const double2 *>(pc.src[j]);
-    double2 *d = reinterpret_cast<double2 *>(pc.dst[j]);
+    const double *s = pc.src[j];
+    double *d = pc.dst[j];
     const long long n2 = pc.PL / 2;
+    const long long r2 = pc.row / 2;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
-         i += (long long)gridDim.x * blockDim.x)
-        d[i] = s[i];
+         i += (long long)gridDim.x * blockDim.x) {
+        long long o = 2 * i;
+        if (r2) o = (i / r2) * pc.stride + 2 * (i % r2);
+        *reinterpret_cast<double2 *>(d + o) = *reinterpret_cast<const double2 *>(s + o);
+    }
 }
 
 static int run_plane_copies(const PlaneCopies &pc, cudaStream_t st) {
@@ -292,14 +303,39 @@ static inline double *plane(double *base, const ltk_slab *s, int comp, long long
     return base + comp * s->cstride + zs * s->nx * s->ny;
 }
 
+// f/g storage layout: element (comp i, storage plane zs, row y, x) at
+// i*SI + zs*SZ + y*SY + x.  SoA (component-major planes) is the C-ABI slab
+// layout; the engine may hold its state row-blocked instead (the 19
+// components of one x-row adjacent), which keeps the pages a CTA touches at
+// once few.
+struct Lay {
+    long long SI, SZ, SY;
+};
+static inline Lay soa_lay(const ltk_slab *s) { return {s->cstride, s->nx * s->ny, s->nx}; }
+static inline Lay row_lay(const ltk_slab *s) { return {s->nx, s->ny * Q * s->nx, Q * s->nx}; }
+static inline bool is_soa(const Lay &L, const ltk_slab *s) { return L.SY == s->nx && L.SI == s->cstride; }
+static inline double *plane(double *base, const Lay &L, int comp, long long zs) {
+    return base + comp * L.SI + zs * L.SZ;
+}
+// the copy geometry of one component plane in layout L
+static inline void plane_geom(PlaneCopies &pc, const Lay &L, const ltk_slab *s) {
+    pc.PL = s->nx * s->ny;
+    if (L.SY == s->nx) {
+        pc.row = pc.stride = 0;
+    } else {
+        pc.row = s->nx;
+        pc.stride = L.SY;
+    }
+}
+
 // ------------------------------------------------------------------ transposes
 // host order site (x*ny + y)*nzg + z  <->  slab (z - z0 + 1)*PL + y*nx + x.
 // 32x32 (x, z) tiles staged in shared memory, both sides coalesced.
 template <bool TO_SLAB>
 __global__ void __launch_bounds__(256) k_transpose(double *slab, double *host, long long nx,
                                                    long long ny, long long nzl, long long nzg,
-                                                   long long z0, long long padded,
-                                                   long long cstride, int ncomp) {
+                                                   long long z0, long long padded, long long SI,
+                                                   long long SZ, long long SY, int ncomp) {
     __shared__ double tile[32][33];
     const int tx = threadIdx.x, ty = threadIdx.y;  // (32, 8)
     const long long xb = (long long)blockIdx.x * 32, zb = (long long)blockIdx.y * 32;
@@ -308,8 +344,7 @@ __global__ void __launch_bounds__(256) k_transpose(double *slab, double *host, l
     const int c = (int)(yc / ny);
     if (c >= ncomp) return;
     double *h = host + (long long)c * padded;
-    double *sl = slab + (long long)c * cstride;
-    const long long PL = nx * ny;
+    double *sl = slab + (long long)c * SI + y * SY;
     if (TO_SLAB) {
         for (int k = ty; k < 32; k += 8) {  // read host: z fastest
             const long long x = xb + k, z = zb + tx;
@@ -318,12 +353,12 @@ __global__ void __launch_bounds__(256) k_transpose(double *slab, double *host, l
         __syncthreads();
         for (int k = ty; k < 32; k += 8) {  // write slab: x fastest
             const long long x = xb + tx, z = zb + k;
-            if (x < nx && z < nzl) sl[(z + 1) * PL + y * nx + x] = tile[tx][k];
+            if (x < nx && z < nzl) sl[(z + 1) * SZ + x] = tile[tx][k];
         }
     } else {
         for (int k = ty; k < 32; k += 8) {
             const long long x = xb + tx, z = zb + k;
-            if (x < nx && z < nzl) tile[tx][k] = sl[(z + 1) * PL + y * nx + x];
+            if (x < nx && z < nzl) tile[tx][k] = sl[(z + 1) * SZ + x];
         }
         __syncthreads();
         for (int k = ty; k < 32; k += 8) {
@@ -333,8 +368,9 @@ __global__ void __launch_bounds__(256) k_transpose(double *slab, double *host, l
     }
 }
 
-static int transpose(const ltk_slab *s, double *slab, double *host, long long padded,
-                     long long nzg, long long z0, int ncomp, bool to_slab, cudaStream_t st) {
+static int transpose(const ltk_slab *s, const Lay &L, double *slab, double *host,
+                     long long padded, long long nzg, long long z0, int ncomp, bool to_slab,
+                     cudaStream_t st) {
     if (z0 < 0 || z0 + s->nzl > nzg) return fail(LTK_ERR_SHAPE, "slab planes outside lattice");
     if (padded < s->nx * s->ny * nzg) return fail(LTK_ERR_SHAPE, "padded < nsites");
     if ((long long)s->ny * ncomp > 65535LL * 65535LL) return fail(LTK_ERR_SHAPE, "too many rows");
@@ -344,10 +380,10 @@ static int transpose(const ltk_slab *s, double *slab, double *host, long long pa
     if (grid.z > 65535) return fail(LTK_ERR_SHAPE, "ny*ncomp exceeds 65535");
     if (to_slab)
         k_transpose<true><<<grid, block, 0, st>>>(slab, host, s->nx, s->ny, s->nzl, nzg, z0,
-                                                  padded, s->cstride, ncomp);
+                                                  padded, L.SI, L.SZ, L.SY, ncomp);
     else
         k_transpose<false><<<grid, block, 0, st>>>(slab, host, s->nx, s->ny, s->nzl, nzg, z0,
-                                                   padded, s->cstride, ncomp);
+                                                   padded, L.SI, L.SZ, L.SY, ncomp);
     LTK_CHECK_LAUNCH("k_transpose");
     return LTK_OK;
 }
@@ -421,6 +457,7 @@ struct ltk_fluid {
     int rank = 0, nranks = 1, vvl = 1;
     ltk_fluid_params prm{};
     ltk_slab slab{};
+    ltk::Lay lay{};  // f/g layout (SoA unless ltk_fluid_set_layout / LTK_LAYOUT=1 chose row-blocked)
     double *fg[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [state][f/g]
     // phi per state in one allocation (phi of state s at phi + s*phi_stride):
     // the fused kernel forms the next state's phi while this step's stays
@@ -479,6 +516,9 @@ static FluidArgs engine_args(const ltk_fluid *e, int in_state) {
     fill_args(a, &e->slab, &e->prm);
     a.nz_global = e->nzg;
     a.z0 = e->z0;
+    a.SI = e->lay.SI;
+    a.SZ = e->lay.SZ;
+    a.SY = e->lay.SY;
     a.f_in = e->fg[in_state][0];
     a.g_in = e->fg[in_state][1];
     a.f_out = e->fg[1 - in_state][0];
@@ -686,19 +726,21 @@ constexpr int kTotBlocks = 592, kTotThreads = 256;
 
 __global__ void __launch_bounds__(kTotThreads) k_totals(const double *f, const double *g,
                                                         long long nx, long long ny, long long nzl,
-                                                        long long cstride, double *partial) {
+                                                        long long SI, long long SZ, long long SY,
+                                                        double *partial) {
     const long long PL = nx * ny, n = PL * nzl;
     double acc[5] = {0, 0, 0, 0, 0};
     for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
-        const long long o = PL + t;  // storage plane 1 onwards
+        const long long z = t / PL, r = t - z * PL, y = r / nx;
+        const long long o = (z + 1) * SZ + y * SY + (r - y * nx);  // storage plane 1 onwards
         static_for<0, Q>([&](auto I) {
-            const double fi = f[I.value * cstride + o];
+            const double fi = f[I.value * SI + o];
             acc[0] += fi;
             if constexpr (cx(I.value) != 0) acc[1] += cx(I.value) * fi;
             if constexpr (cy(I.value) != 0) acc[2] += cy(I.value) * fi;
             if constexpr (cz(I.value) != 0) acc[3] += cz(I.value) * fi;
-            acc[4] += g[I.value * cstride + o];
+            acc[4] += g[I.value * SI + o];
         });
     }
     __shared__ double red[5][kTotThreads];
@@ -841,14 +883,14 @@ static int peer_before_load(ltk_fluid *e, cudaStream_t st) {
 static int peer_prime(ltk_fluid *e, int s, cudaStream_t st) {
     PlaneCopies pc;
     memset(&pc, 0, sizeof pc);
-    pc.PL = e->nx * e->ny;
-    const ltk_slab *sl = &e->slab;
+    plane_geom(pc, e->lay, &e->slab);
+    const Lay &L = e->lay;
     for (int j = 0; j < 5; ++j)
         for (int d = 0; d < 2; ++d) {
-            pc.src[pc.n] = plane(e->fg[s][d], sl, kUp[j], e->nzl);
-            pc.dst[pc.n++] = plane(e->up.fg[s][d], sl, kUp[j], 0);
-            pc.src[pc.n] = plane(e->fg[s][d], sl, kDown[j], 1);
-            pc.dst[pc.n++] = plane(e->dn.fg[s][d], sl, kDown[j], e->nzl + 1);
+            pc.src[pc.n] = plane(e->fg[s][d], L, kUp[j], e->nzl);
+            pc.dst[pc.n++] = plane(e->up.fg[s][d], L, kUp[j], 0);
+            pc.src[pc.n] = plane(e->fg[s][d], L, kDown[j], 1);
+            pc.dst[pc.n++] = plane(e->dn.fg[s][d], L, kDown[j], e->nzl + 1);
         }
     LTK_RC(run_plane_copies(pc, st));
     e->primed = true;
@@ -921,8 +963,27 @@ static int preload_step_kernels() {
 }
 
 static int wrap_state_halos(ltk_fluid *e, int s, int which, cudaStream_t st) {
-    return ltk_fluid_wrap_halos(&e->slab, e->fg[s][0], e->fg[s][1], e->phi_of(s), e->mu, which,
-                                st);
+    if (is_soa(e->lay, &e->slab))
+        return ltk_fluid_wrap_halos(&e->slab, e->fg[s][0], e->fg[s][1], e->phi_of(s), e->mu,
+                                    which, st);
+    if (which & 1) {  // row-blocked f/g: the crossing components' periodic images
+        PlaneCopies pc;
+        memset(&pc, 0, sizeof pc);
+        plane_geom(pc, e->lay, &e->slab);
+        for (int j = 0; j < 5; ++j)
+            for (int d = 0; d < 2; ++d) {
+                double *b = e->fg[s][d];
+                pc.src[pc.n] = plane(b, e->lay, kUp[j], e->nzl);
+                pc.dst[pc.n++] = plane(b, e->lay, kUp[j], 0);
+                pc.src[pc.n] = plane(b, e->lay, kDown[j], 1);
+                pc.dst[pc.n++] = plane(b, e->lay, kDown[j], e->nzl + 1);
+            }
+        LTK_RC(run_plane_copies(pc, st));
+    }
+    if (which & 6)
+        return ltk_fluid_wrap_halos(&e->slab, e->fg[s][0], e->fg[s][1], e->phi_of(s), e->mu,
+                                    which & 6, st);
+    return LTK_OK;
 }
 
 }  // namespace ltk
@@ -1041,14 +1102,14 @@ int ltk_fluid_unpack_face(const ltk_slab *s, double *f, double *g, const double 
 int ltk_fluid_scatter(const ltk_slab *s, const double *host, int64_t padded, int64_t nz_global,
                       int64_t z0, int32_t ncomp, double *slab, void *stream) {
     LTK_RC(check_slab(s, 1));
-    return transpose(s, slab, const_cast<double *>(host), padded, nz_global, z0, ncomp, true,
+    return transpose(s, soa_lay(s), slab, const_cast<double *>(host), padded, nz_global, z0, ncomp, true,
                      as_stream(stream));
 }
 
 int ltk_fluid_gather(const ltk_slab *s, const double *slab, int64_t padded, int64_t nz_global,
                      int64_t z0, int32_t ncomp, double *host, void *stream) {
     LTK_RC(check_slab(s, 1));
-    return transpose(s, const_cast<double *>(slab), host, padded, nz_global, z0, ncomp, false,
+    return transpose(s, soa_lay(s), const_cast<double *>(slab), host, padded, nz_global, z0, ncomp, false,
                      as_stream(stream));
 }
 
@@ -1135,6 +1196,11 @@ int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank, in
         return rc;
     }
     e->fsync = (unsigned long long *)ptr;
+    // row-blocked f/g by default (measured faster, bitwise identical: DESIGN.md §4);
+    // SoA for odd nx (16-byte rows) or LTK_LAYOUT=0
+    e->lay = nx % 2 == 0 ? row_lay(&e->slab) : soa_lay(&e->slab);
+    if (const char *v = getenv("LTK_LAYOUT"))
+        if (atoi(v) == LTK_LAYOUT_SOA) e->lay = soa_lay(&e->slab);
     if (const char *v = getenv("LTK_FUSE")) e->fuse = atoi(v) != 0;  // default off
     if (const char *v = getenv("LTK_PEER_OVERLAP")) e->peer_overlap = atoi(v) != 0;
     if (const char *v = getenv("LTK_FUSE_LAG")) e->fuse_lag = std::max(0, atoi(v));
@@ -1234,8 +1300,10 @@ int ltk_fluid_load(ltk_fluid *e, const double *f_src, const double *g_src, int64
     if (e->transport == kPeer) LTK_RC(peer_before_load(e, st));
     e->cur = 0;
     e->phi_lo = e->phi_hi = 0;  // phi of the loaded state not formed yet
-    LTK_RC(ltk_fluid_scatter(&e->slab, f_src, padded, nz_src, z_src0, Q, e->fg[0][0], st));
-    LTK_RC(ltk_fluid_scatter(&e->slab, g_src, padded, nz_src, z_src0, Q, e->fg[0][1], st));
+    LTK_RC(transpose(&e->slab, e->lay, e->fg[0][0], const_cast<double *>(f_src), padded, nz_src,
+                     z_src0, Q, true, st));
+    LTK_RC(transpose(&e->slab, e->lay, e->fg[0][1], const_cast<double *>(g_src), padded, nz_src,
+                     z_src0, Q, true, st));
     if (e->transport == kLocal) LTK_RC(wrap_state_halos(e, 0, 1, st));
     if (e->transport == kPeer) LTK_RC(peer_prime(e, 0, st));
     return LTK_OK;
@@ -1244,8 +1312,10 @@ int ltk_fluid_load(ltk_fluid *e, const double *f_src, const double *g_src, int64
 int ltk_fluid_store(ltk_fluid *e, double *f_dst, double *g_dst, int64_t padded, int64_t nz_src,
                     int64_t z_src0, void *stream) {
     cudaStream_t st = stream ? as_stream(stream) : e->st;
-    LTK_RC(ltk_fluid_gather(&e->slab, e->fg[e->cur][0], padded, nz_src, z_src0, Q, f_dst, st));
-    LTK_RC(ltk_fluid_gather(&e->slab, e->fg[e->cur][1], padded, nz_src, z_src0, Q, g_dst, st));
+    LTK_RC(transpose(&e->slab, e->lay, e->fg[e->cur][0], f_dst, padded, nz_src, z_src0, Q, false,
+                     st));
+    LTK_RC(transpose(&e->slab, e->lay, e->fg[e->cur][1], g_dst, padded, nz_src, z_src0, Q, false,
+                     st));
     return LTK_OK;
 }
 
@@ -1253,7 +1323,8 @@ int ltk_fluid_totals(ltk_fluid *e, double *out5) {
     double *partial = nullptr;
     LTK_CUDA(cudaMallocAsync(&partial, sizeof(double) * 5 * kTotBlocks, e->st));
     k_totals<<<kTotBlocks, kTotThreads, 0, e->st>>>(e->fg[e->cur][0], e->fg[e->cur][1], e->nx,
-                                                   e->ny, e->nzl, e->slab.cstride, partial);
+                                                   e->ny, e->nzl, e->lay.SI, e->lay.SZ,
+                                                   e->lay.SY, partial);
     LTK_CHECK_LAUNCH("k_totals");
     std::vector<double> h(5 * kTotBlocks);
     LTK_CUDA(cudaMemcpyAsync(h.data(), partial, sizeof(double) * h.size(),
@@ -1364,6 +1435,7 @@ int ltk_fluid_set_fuse(ltk_fluid *e, int32_t enable, int32_t extra_lag) {
 struct IpcBlob {
     cudaIpcMemHandle_t h[7];  // f0 g0 f1 g1 phi mu inbox
     unsigned long long off[7];
+    long long SY;  // f/g layout (row stride) of the exporting slab
 };
 static_assert(sizeof(IpcBlob) <= LTK_IPC_BLOB_BYTES, "IPC blob too large");
 
@@ -1395,6 +1467,7 @@ int ltk_fluid_ipc_blob(ltk_fluid *e, char *blob) {
         LTK_CUDA(cudaIpcGetMemHandle(&b.h[k], ptrs[k]));
         LTK_RC(alloc_base(ptrs[k], &b.off[k]));
     }
+    b.SY = e->lay.SY;
     memset(blob, 0, LTK_IPC_BLOB_BYTES);
     memcpy(blob, &b, sizeof b);
     return LTK_OK;
@@ -1403,6 +1476,7 @@ int ltk_fluid_ipc_blob(ltk_fluid *e, char *blob) {
 static int open_peer(ltk_fluid *e, const char *blob, ltk_fluid::Peer &p) {
     IpcBlob b;
     memcpy(&b, blob, sizeof b);
+    if (b.SY != e->lay.SY) return fail(LTK_ERR_SHAPE, "peer slabs differ in layout");
     char *ptrs[7];
     for (int k = 0; k < 7; ++k) {
         void *base = nullptr;
@@ -1459,7 +1533,8 @@ static void peer_from_engine(ltk_fluid::Peer &p, const ltk_fluid *o) {
 int ltk_fluid_attach_peer_engines(ltk_fluid *e, const ltk_fluid *up, const ltk_fluid *dn) {
     if (e->nranks < 2) return fail(LTK_ERR_CONFIG, "peer transport needs >= 2 slabs");
     if (e->transport != kLocal) return fail(LTK_ERR_CONFIG, "transport already attached");
-    if (up->slab.cstride != e->slab.cstride || dn->slab.cstride != e->slab.cstride)
+    if (up->slab.cstride != e->slab.cstride || dn->slab.cstride != e->slab.cstride ||
+        up->lay.SY != e->lay.SY || dn->lay.SY != e->lay.SY)
         return fail(LTK_ERR_SHAPE, "peer slabs differ in layout");
     LTK_RC(preload_step_kernels());
     preload_cs_tma((int)e->nx);
@@ -1514,6 +1589,11 @@ int ltk_nccl_unique_id(char id[128]) {
 
 int ltk_fluid_attach_nccl(ltk_fluid *e, const char id[128]) {
     if (!nccl().ok) return fail(LTK_ERR_DEVICE, "libnccl.so.2 not loadable");
+    if (!is_soa(e->lay, &e->slab)) {  // NCCL sends contiguous SoA component planes
+        e->lay = soa_lay(&e->slab);
+        e->cur = 0;
+        e->phi_lo = e->phi_hi = 0;
+    }
     ncclUniqueId u;
     memcpy(u.internal, id, 128);
     LTK_NCCL(nccl().CommInitRank(&e->comm, e->nranks, u, e->rank));
@@ -1523,3 +1603,19 @@ int ltk_fluid_attach_nccl(ltk_fluid *e, const char id[128]) {
 }
 
 }  // extern "C"
+
+extern "C" int ltk_fluid_set_layout(ltk_fluid *e, int32_t layout, int32_t *previous) {
+    if (previous) *previous = is_soa(e->lay, &e->slab) ? LTK_LAYOUT_SOA : LTK_LAYOUT_ROW;
+    if (layout < 0) return LTK_OK;  // query
+    if (layout != LTK_LAYOUT_SOA && layout != LTK_LAYOUT_ROW)
+        return fail(LTK_ERR_CONFIG, "unknown layout %d", layout);
+    if (e->transport != kLocal)
+        return fail(LTK_ERR_CONFIG, "set the layout before attaching a transport");
+    if (layout == LTK_LAYOUT_ROW && e->nx % 2)
+        return fail(LTK_ERR_SHAPE, "the row-blocked layout needs an even nx");
+    e->lay = layout == LTK_LAYOUT_ROW ? row_lay(&e->slab) : soa_lay(&e->slab);
+    e->cur = 0;
+    e->phi_lo = e->phi_hi = 0;
+    drop_graphs(e);
+    return LTK_OK;
+}

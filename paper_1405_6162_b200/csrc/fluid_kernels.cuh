@@ -48,6 +48,9 @@ struct FluidArgs {
     double *img_f_up, *img_g_up, *img_f_dn, *img_g_dn;
     double *img_phi_up, *img_phi_dn, *img_mu_up, *img_mu_dn;
     long long PL, cstride;
+    // f/g element (component i, storage plane zs, row y, x) at i*SI + zs*SZ + y*SY + x:
+    // SoA (SI, SZ, SY) = (cstride, PL, nx); row-blocked (nx, ny*Q*nx, Q*nx)
+    long long SI, SZ, SY;
     long long nthreads;   // threads of this launch
     long long nz_global, z0;  // for error-site reporting in host order
     // fused collide-stream + next-state phi (k_cs_phi); see that kernel
@@ -99,8 +102,8 @@ template <int I, int VVL, int LD = kLdg>
 __device__ __forceinline__ void pull(double (&v)[VVL], const double *base, const FluidArgs &a,
                                      const Pos &p, uint64_t pol = 0) {
     const int ys = wrapi(p.y - cy(I), a.ny);
-    const double *row = base + (long long)I * a.cstride +
-                        (long long)(p.z + 1 - cz(I)) * a.PL + (long long)ys * a.nx;
+    const double *row = base + (long long)I * a.SI + (long long)(p.z + 1 - cz(I)) * a.SZ +
+                        (long long)ys * a.SY;
     if constexpr (cx(I) == 0) {
         if constexpr (LD == kLdg) load_vec<VVL>(v, row + p.x0);
         else if constexpr (LD == kLdNc) load_vec_nc<VVL>(v, row + p.x0, pol);
@@ -487,28 +490,28 @@ __device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, doub
             if (ok[k]) frelax_pair<C, MODE, PHYS, T1, VVL>(F, G, k, st[k], a);
     });
 
-    const long long off = (long long)p.y * a.nx + p.x0;
-    const long long o = (long long)(p.z + 1) * a.PL + off;
+    const long long off = (long long)p.y * a.SY + p.x0;       // row offset inside a plane
+    const long long o = (long long)(p.z + 1) * a.SZ + off;
     static_for<0, Q>([&](auto I) {
         if constexpr (HINT & 2) {
-            store_vec_pol<VVL>(a.f_out + I.value * a.cstride + o, F[I.value], pol_first);
-            store_vec_pol<VVL>(a.g_out + I.value * a.cstride + o, G[I.value], pol_last);
+            store_vec_pol<VVL>(a.f_out + I.value * a.SI + o, F[I.value], pol_first);
+            store_vec_pol<VVL>(a.g_out + I.value * a.SI + o, G[I.value], pol_last);
         } else {
-            store_vec<VVL>(a.f_out + I.value * a.cstride + o, F[I.value]);
-            store_vec<VVL>(a.g_out + I.value * a.cstride + o, G[I.value]);
+            store_vec<VVL>(a.f_out + I.value * a.SI + o, F[I.value]);
+            store_vec<VVL>(a.g_out + I.value * a.SI + o, G[I.value]);
         }
         // halo images of the components that cross the z faces
         if constexpr (cz(I.value) < 0) {
             if (p.z == 0 && a.img_f_dn) {
-                const long long h = (long long)(a.nzl + 1) * a.PL + off;
-                store_vec<VVL>(a.img_f_dn + I.value * a.cstride + h, F[I.value]);
-                store_vec<VVL>(a.img_g_dn + I.value * a.cstride + h, G[I.value]);
+                const long long h = (long long)(a.nzl + 1) * a.SZ + off;
+                store_vec<VVL>(a.img_f_dn + I.value * a.SI + h, F[I.value]);
+                store_vec<VVL>(a.img_g_dn + I.value * a.SI + h, G[I.value]);
             }
         }
         if constexpr (cz(I.value) > 0) {
             if (p.z == a.nzl - 1 && a.img_f_up) {
-                store_vec<VVL>(a.img_f_up + I.value * a.cstride + off, F[I.value]);
-                store_vec<VVL>(a.img_g_up + I.value * a.cstride + off, G[I.value]);
+                store_vec<VVL>(a.img_f_up + I.value * a.SI + off, F[I.value]);
+                store_vec<VVL>(a.img_g_up + I.value * a.SI + off, G[I.value]);
             }
         }
     });

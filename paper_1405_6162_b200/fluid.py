@@ -34,6 +34,7 @@ MODE_FAST = nat.MODE_FAST
 CS_REG = nat.CS_REG
 CS_TMA = nat.CS_TMA
 MU_AUTO, MU_TMA, MU_PLAIN = nat.MU_AUTO, nat.MU_TMA, nat.MU_PLAIN
+LAYOUT_SOA, LAYOUT_ROW = nat.LAYOUT_SOA, nat.LAYOUT_ROW
 #: passive: the reference collision after streaming; binary: free-energy binary
 #: fluid with the force F = -phi grad(mu); binary-stress: the same fluid with the
 #: momentum-conserving F = -div P of the chemical pressure tensor (stable flat
@@ -168,10 +169,22 @@ class BinaryFluid:
         nat.check(nat.lib.ltk_fluid_use_graph(self._h, 1 if enable else 0), "use_graph")
 
     def set_fuse(self, enable: bool, extra_lag: int = 1) -> None:
-        """Fused collide-stream + next-state phi (k_cs_phi; on by default).
-        Bitwise identical either way; off runs the three-kernel step."""
+        """Fused collide-stream + next-state phi (k_cs_phi; off by default, it
+        measured slower).  Bitwise identical either way; off runs the
+        three-kernel step."""
         nat.check(nat.lib.ltk_fluid_set_fuse(self._h, 1 if enable else 0, int(extra_lag)),
                   "set_fuse")
+
+    def set_layout(self, layout: int | None = None) -> int:
+        """f/g storage layout of this slab: LAYOUT_ROW (row-blocked: the 19
+        components of an x-row adjacent; default for even nx, measured faster)
+        or LAYOUT_SOA (component-major planes; attach_nccl selects it).
+        Bitwise identical results; set before load() and before attaching a
+        transport.  Returns the previous layout (None only queries)."""
+        prev = ctypes.c_int32()
+        nat.check(nat.lib.ltk_fluid_set_layout(self._h, -1 if layout is None else int(layout),
+                                               ctypes.byref(prev)), "set_layout")
+        return prev.value
 
     def ipc_blob(self) -> bytes:
         """CUDA IPC handles of this slab's buffers (exchange them, then attach_peers)."""

@@ -11,6 +11,7 @@ equal to the single-slab run.
 """
 
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -584,3 +585,84 @@ class TestRandomShapes:
             assert np.array_equal(g1.data.view(np.uint64), og.view(np.uint64)), shape
 
         check()
+
+
+class TestRowLayout:
+    """The engine's row-blocked f/g layout (LTK_LAYOUT_ROW: the 19 components
+    of an x-row adjacent) against the SoA layout and the oracle: bitwise for
+    every physics, mode, VVL, graph on/off and the fused step; load/store,
+    totals and the periodic images go through the same strides."""
+
+    @staticmethod
+    def _run(lk, shape, layout, physics="binary", mode=None, vvl=1, graph=True, fuse=False,
+             steps=4, seed=23):
+        f0, g0 = _state(lk, shape, seed)
+        model = lk.D3Q19Model(tau_f=0.9, tau_g=1.2)
+        mode = lk.MODE_EXACT if mode is None else mode
+        with lk.BinaryFluid(lk.LatticeShape(*shape), model=model, physics=physics, mode=mode,
+                            vvl=vvl, use_graph=graph) as sim:
+            default = lk.LAYOUT_SOA if os.environ.get("LTK_LAYOUT") == "0" else lk.LAYOUT_ROW
+            assert sim.set_layout(layout) == default  # row-blocked for even nx
+            assert sim.set_layout(None) == layout
+            sim.set_fuse(fuse, 1)
+            sim.load(f0, g0)
+            sim.run(steps)
+            f1, g1 = sim.fields()
+            phi, mu = sim.order_parameter()
+            tot = sim.totals()
+        return f0, g0, (f1.data, g1.data, phi, mu, tot)
+
+    @pytest.mark.parametrize("physics", ["binary", "passive", "binary-stress"])
+    @pytest.mark.parametrize("shape", [(16, 12, 10), (32, 16, 6), (6, 10, 4), (64, 3, 9)])
+    def test_row_matches_oracle(self, lk, shape, physics):
+        f0, g0, got = self._run(lk, shape, lk.LAYOUT_ROW, physics)
+        ph = {"passive": 0, "binary": 1, "binary-stress": 2}[physics]
+        of, og, _, _ = _oracle(f0, g0, shape, 4, ph, 0.9, 1.2)
+        assert np.array_equal(got[0].view(np.uint64), of.view(np.uint64))
+        assert np.array_equal(got[1].view(np.uint64), og.view(np.uint64))
+
+    @pytest.mark.parametrize("physics", ["binary", "binary-stress"])
+    @pytest.mark.parametrize("vvl,graph,fuse", [(1, False, False), (2, True, False),
+                                                (1, True, True), (2, False, True)])
+    def test_row_equals_soa(self, lk, physics, vvl, graph, fuse):
+        shape = (32, 12, 14)
+        for mode in (lk.MODE_EXACT, lk.MODE_FAST):
+            fz = fuse and physics != "binary-stress"
+            _, _, ref = self._run(lk, shape, lk.LAYOUT_SOA, physics, mode, vvl, graph, fz)
+            _, _, got = self._run(lk, shape, lk.LAYOUT_ROW, physics, mode, vvl, graph, fz)
+            for a, b in zip(got, ref):
+                assert np.array_equal(np.asarray(a).view(np.uint64),
+                                      np.asarray(b).view(np.uint64)), (mode, vvl, graph, fz)
+
+    def test_row_large_plane_fast(self, lk):
+        # BASELINE plane size; TMA requested but SoA-only: the register kernel runs
+        shape = (256, 256, 12)
+        prev = lk.cs_variant(lk.CS_TMA)
+        try:
+            _, _, got = self._run(lk, shape, lk.LAYOUT_ROW, mode=lk.MODE_FAST, steps=3)
+        finally:
+            lk.cs_variant(prev)
+        _, _, ref = self._run(lk, shape, lk.LAYOUT_SOA, mode=lk.MODE_FAST, steps=3)
+        for a, b in zip(got, ref):
+            assert np.array_equal(a, b)
+
+    def test_row_layout_rules(self, lk):
+        with lk.BinaryFluid(lk.LatticeShape(7, 4, 4)) as sim:
+            assert sim.set_layout(None) == lk.LAYOUT_SOA  # odd nx keeps SoA
+            with pytest.raises(lk.ShapeError):
+                sim.set_layout(lk.LAYOUT_ROW)  # odd nx
+            with pytest.raises(lk.ConfigError):
+                sim.set_layout(5)
+        a = lk.BinaryFluid(lk.LatticeShape(16, 4, 8), rank=0, nranks=2)
+        b = lk.BinaryFluid(lk.LatticeShape(16, 4, 8), rank=1, nranks=2)
+        try:
+            a.set_layout(lk.LAYOUT_SOA)
+            with pytest.raises(lk.ShapeError):
+                a.attach_peer_engines(b, b)  # layouts differ
+            a.set_layout(lk.LAYOUT_ROW)
+            a.attach_peer_engines(b, b)
+            with pytest.raises(lk.ConfigError):
+                a.set_layout(lk.LAYOUT_SOA)  # after attaching a transport
+        finally:
+            a.close()
+            b.close()

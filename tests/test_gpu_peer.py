@@ -37,7 +37,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, shape, steps, physics, q):
+def _worker(rank, world, port, shape, steps, physics, q, layout=0):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -55,6 +55,7 @@ def _worker(rank, world, port, shape, steps, physics, q):
         model = lk.D3Q19Model(tau_f=0.9, tau_g=1.1)
         sim = lk.BinaryFluid(full, model=model, physics=physics, rank=rank, nranks=world,
                              use_graph=False)
+        sim.set_layout(layout)
         blob = torch.frombuffer(bytearray(sim.ipc_blob()), dtype=torch.uint8)
         blobs = [torch.zeros_like(blob) for _ in range(world)]
         dist.all_gather(blobs, blob)
@@ -91,11 +92,12 @@ def _worker(rank, world, port, shape, steps, physics, q):
 
 
 # variant: "plain" (three-kernel step), "fused" (k_cs_phi on the interior planes
-# of every slab; needs nzl >= 5), "tma" (k_cs_tma; nx a multiple of 128)
+# of every slab; needs nzl >= 5), "tma" (k_cs_tma; nx a multiple of 128), "row*" (the
+# row-blocked f/g layout, plain and fused)
 @pytest.mark.parametrize("nslabs", [2, 3, 4])
 @pytest.mark.parametrize("physics", ["binary", "passive", "binary-stress"])
 @pytest.mark.parametrize("nz,variant", [(12, "plain"), (24, "plain"), (24, "fused"), (24, "tma"),
-                                        (12, "vvl2")])
+                                        (12, "vvl2"), (24, "row"), (24, "row-fused")])
 def test_engines_in_one_process_bitwise(nslabs, physics, nz, variant):
     import paper_1405_6162_b200 as lk
     from oracle import oracle as orc
@@ -109,7 +111,8 @@ def test_engines_in_one_process_bitwise(nslabs, physics, nz, variant):
                            use_graph=False, vvl=2 if variant == "vvl2" else 1)
             for r in range(nslabs)]
     for sim in sims:
-        sim.set_fuse(variant == "fused", 1)
+        sim.set_fuse(variant.endswith("fused"), 1)
+        sim.set_layout(lk.LAYOUT_ROW if variant.startswith("row") else lk.LAYOUT_SOA)
     try:
         for r, sim in enumerate(sims):
             sim.attach_peer_engines(sims[(r + 1) % nslabs], sims[(r - 1) % nslabs])
@@ -144,15 +147,15 @@ def test_engines_in_one_process_bitwise(nslabs, physics, nz, variant):
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-@pytest.mark.parametrize("physics", ["binary", "passive"])
-def test_two_process_peer_slabs_bitwise(physics):
+@pytest.mark.parametrize("physics,layout", [("binary", 0), ("passive", 0), ("binary", 1)])
+def test_two_process_peer_slabs_bitwise(physics, layout):
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
     shape, steps = (16, 8, 12), 3
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, shape, steps, physics, q))
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, shape, steps, physics, q, layout))
              for r in range(2)]
     for p in procs:
         p.start()
