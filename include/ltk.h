@@ -258,12 +258,15 @@ int ltk_fluid_set_fuse(ltk_fluid *e, int32_t enable, int32_t extra_lag);
 #define LTK_CS_TMA 1
 int ltk_fluid_cs_variant(int32_t variant, int32_t *previous);
 /* Chemical-potential stencil kernel, process-wide: LTK_MU_AUTO = register
- * 2.5-D column kernel k_mu_col (nx % 32 == 0, ny % 8 == 0), else the TMA
- * shared-memory kernel k_mu_tma, else k_mu; LTK_MU_TMA skips k_mu_col;
- * LTK_MU_PLAIN forces k_mu.  Bitwise identical.  variant < 0 only queries. */
+ * 2.5-D block kernel k_mu_blk (nx % 32 == 0, ny % 8 == 0; 8 planes of centre
+ * loads in flight per thread), else the TMA shared-memory kernel k_mu_tma,
+ * else k_mu; LTK_MU_COL = the marching column kernel k_mu_col in k_mu_blk's
+ * place; LTK_MU_TMA skips the register kernels; LTK_MU_PLAIN forces k_mu.
+ * Bitwise identical.  variant < 0 only queries. */
 #define LTK_MU_AUTO 0
 #define LTK_MU_TMA 1
 #define LTK_MU_PLAIN 2
+#define LTK_MU_COL 3
 int ltk_fluid_mu_variant(int32_t variant, int32_t *previous);
 
 /* f/g storage layout of an engine.  LTK_LAYOUT_SOA: component-major

@@ -98,8 +98,9 @@ static int launch_phi(const FluidArgs &a, int vvl, cudaStream_t st) {
     return LTK_OK;
 }
 
-// mu stencil kernel (process-wide): LTK_MU_AUTO = k_mu_col where it applies,
-// else k_mu_tma, else k_mu; LTK_MU_TMA skips k_mu_col; LTK_MU_PLAIN = k_mu.
+// mu stencil kernel (process-wide): LTK_MU_AUTO = k_mu_blk where it applies,
+// else k_mu_tma, else k_mu; LTK_MU_COL = k_mu_col in k_mu_blk's place;
+// LTK_MU_TMA skips both register kernels; LTK_MU_PLAIN = k_mu.
 static int &mu_variant() {
     static int v = LTK_MU_AUTO;
     return v;
@@ -108,7 +109,14 @@ static int &mu_variant() {
 static int launch_mu(const FluidArgs &a, int vvl, cudaStream_t st) {
     if (a.nthreads <= 0) return LTK_OK;
     const int variant = mu_variant();
-    if (variant == LTK_MU_AUTO && mu_col_ok(a)) {
+    if ((variant == LTK_MU_AUTO || variant == LTK_MU_COL) && mu_col_ok(a)) {
+        if (variant == LTK_MU_AUTO) {
+            dim3 grid((unsigned)(a.nx / 32), (unsigned)(a.ny / 8),
+                      (unsigned)((a.nplanes + kMuBlkZ - 1) / kMuBlkZ));
+            k_mu_blk<kMuBlkZ><<<grid, dim3(32, 8), 0, st>>>(a);
+            LTK_CHECK_LAUNCH("k_mu_blk");
+            return LTK_OK;
+        }
         dim3 grid((unsigned)(a.nx / 32), (unsigned)(a.ny / 8),
                   (unsigned)((a.nplanes + kMuColZ - 1) / kMuColZ));
         k_mu_col<><<<grid, dim3(32, 8), 0, st>>>(a);
@@ -935,6 +943,7 @@ static int preload_step_kernels() {
     cudaFuncGetAttributes(&fa, k_mu<2>);
     cudaFuncGetAttributes(&fa, k_mu<4>);
     cudaFuncGetAttributes(&fa, k_mu_col<>);
+    cudaFuncGetAttributes(&fa, k_mu_blk<kMuBlkZ>);
     cudaFuncGetAttributes(&fa, k_mu_tma<4>);
     cudaFuncGetAttributes(&fa, k_mu_tma<2>);
     cudaFuncGetAttributes(&fa, k_plane_copy);
@@ -1571,7 +1580,7 @@ int ltk_fluid_cs_variant(int32_t variant, int32_t *previous) {
 int ltk_fluid_mu_variant(int32_t variant, int32_t *previous) {
     if (previous) *previous = mu_variant();
     if (variant >= 0) {
-        if (variant > LTK_MU_PLAIN) return fail(LTK_ERR_CONFIG, "unknown mu variant %d", variant);
+        if (variant > LTK_MU_COL) return fail(LTK_ERR_CONFIG, "unknown mu variant %d", variant);
         mu_variant() = variant;
     }
     return LTK_OK;

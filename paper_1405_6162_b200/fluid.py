@@ -33,7 +33,7 @@ MODE_EXACT = nat.MODE_EXACT
 MODE_FAST = nat.MODE_FAST
 CS_REG = nat.CS_REG
 CS_TMA = nat.CS_TMA
-MU_AUTO, MU_TMA, MU_PLAIN = nat.MU_AUTO, nat.MU_TMA, nat.MU_PLAIN
+MU_AUTO, MU_TMA, MU_PLAIN, MU_COL = nat.MU_AUTO, nat.MU_TMA, nat.MU_PLAIN, nat.MU_COL
 LAYOUT_SOA, LAYOUT_ROW = nat.LAYOUT_SOA, nat.LAYOUT_ROW
 #: passive: the reference collision after streaming; binary: free-energy binary
 #: fluid with the force F = -phi grad(mu); binary-stress: the same fluid with the
@@ -338,7 +338,8 @@ def cs_variant(variant: int | None = None) -> int:
 
 def mu_variant(variant: int | None = None) -> int:
     """Chemical-potential stencil kernel of the process: MU_AUTO (register
-    column kernel where it applies, else TMA, else plain), MU_TMA, MU_PLAIN.
+    block kernel k_mu_blk where it applies, else TMA, else plain), MU_COL
+    (the marching column kernel instead of k_mu_blk), MU_TMA, MU_PLAIN.
     Returns the previous value; None only queries."""
     prev = ctypes.c_int32(0)
     nat.check(nat.lib.ltk_fluid_mu_variant(-1 if variant is None else int(variant),
