@@ -220,8 +220,8 @@ __global__ void __launch_bounds__(256) k_mu_col(const FluidArgs a) {
 // 0.092 ms vs k_mu_col's 0.099; ZC = 16 (80 regs), prefetching the next
 // plane's neighbours (70 regs) or batching the block's outer y rows (78 regs)
 // all lose occupancy and run 0.097-0.12 ms.
-template <int ZC>
-__global__ void __launch_bounds__(256) k_mu_blk(const FluidArgs a) {
+template <int ZC, int MINB = 5>  // 5 blocks/SM: 48 regs (0.091 ms; 4: 62 regs 0.094, 6: spills 0.105)
+__global__ void __launch_bounds__(256, MINB) k_mu_blk(const FluidArgs a) {
     const int lane = threadIdx.x, nx = a.nx;
     const int x = blockIdx.x * 32 + lane, y = blockIdx.y * 8 + threadIdx.y;
     const int zb = a.z_lo + blockIdx.z * ZC;
