@@ -119,18 +119,19 @@ struct Exact {
 // exact in one FMA, and RN(q + e r) == RN(x / d) whenever nothing overflows or
 // underflows.  So this is bitwise __ddiv_rn(x, d) for the lattice's operands
 // in 3 dependent FP64 ops instead of the ~10-op, branchy division sequence.
-// Edge cases (d > 0 finite everywhere here): a zero quotient keeps the sign of
-// x (x is then +-0), an infinite x passes through, NaN stays NaN.
-// The guard tests x's bit pattern on the integer pipe (exponent all ones:
-// inf/NaN -> x; all bits but the sign zero: +-0 -> x) so the division costs
-// exactly three FP64-pipe instructions.
+// Edge cases (d > 0 finite everywhere here): the remainder is formed negated,
+// en = q d - x, and the result as q - en r, so a zero x comes out with its own
+// sign by plain IEEE arithmetic (x = -0: q = -0, en = +0, -0 + -0 = -0; x = +0:
+// +0), and for every other x en = -e exactly, i.e. the same correctly rounded
+// q + e r.  Only inf/NaN x (exponent all ones) need the pass-through, tested
+// on the high word on the integer pipe: 3 FP64 instructions plus a LOP3, an
+// ISETP and the 64-bit select per division.
 __device__ __forceinline__ double div_rcp(double x, double d, double r) {
     const double q = __dmul_rn(x, r);
-    const double e = __fma_rn(-q, d, x);
-    const double res = __fma_rn(e, r, q);
-    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
-    const bool pass = ((b >> 52) & 0x7ffull) == 0x7ffull || (b << 1) == 0ull;
-    return pass ? x : res;
+    const double en = __fma_rn(q, d, -x);
+    const double res = __fma_rn(-en, r, q);
+    const unsigned hi = (unsigned)__double2hiint(x);
+    return (hi & 0x7ff00000u) == 0x7ff00000u ? x : res;
 }
 
 // FAST: plain operators (the compiler may contract to FMA).
