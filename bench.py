@@ -96,10 +96,11 @@ def parse_args(argv=None):
                         "three-kernel step")
     p.add_argument("--fuse-lag", type=int, default=1,
                    help="planes of slack between the collision and phi fronts of k_cs_phi")
-    p.add_argument("--layout", choices=("soa", "row"), default="row",
+    p.add_argument("--layout", choices=("soa", "row"), default=None,
                    help="f/g storage: component-major planes (soa) or row-blocked (row: "
                         "the 19 components of an x-row adjacent); bitwise identical. "
-                        "The NCCL transport always uses soa")
+                        "The NCCL transport always uses soa; default row, soa with --fuse "
+                        "(measured faster for each)")
     p.add_argument("--transport", choices=("peer", "nccl"), default="peer",
                    help="N>1 halo exchange: peer stores from the kernels (CUDA IPC over "
                         "NVLink) or NCCL send/recv")
@@ -337,7 +338,8 @@ def run_ours(args, rank, world, local):
                          rank=rank, nranks=world, device=local, use_graph=False)
     fused = args.fuse
     sim.set_fuse(fused, args.fuse_lag)
-    sim.set_layout(lk.LAYOUT_ROW if args.layout == "row" else lk.LAYOUT_SOA)
+    want = args.layout or ("soa" if fused else "row")
+    sim.set_layout(lk.LAYOUT_ROW if want == "row" else lk.LAYOUT_SOA)
     if world > 1 and args.transport == "nccl":
         uid = lk.nccl_unique_id() if rank == 0 else None
         sim.attach_nccl(ctl.bcast_bytes(uid, 128))
