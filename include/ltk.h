@@ -221,7 +221,10 @@ int ltk_fluid_create(int64_t nx, int64_t ny, int64_t nz_global, int32_t rank,
                      ltk_fluid **out);
 int ltk_fluid_destroy(ltk_fluid *e);
 int ltk_fluid_slab(const ltk_fluid *e, ltk_slab *s, int64_t *z0);
-/* Device pointers of the current state (post-collision f, g) and of phi/mu. */
+/* Device pointers of the current state (post-collision f, g) and of phi/mu.
+ * f/g are in the engine's layout (ltk_fluid_set_layout: row-blocked by
+ * default for even nx, not the ltk_slab SoA layout); ltk_fluid_store gives
+ * them in host order.  phi/mu are plane-major (zs*nx*ny + y*nx + x). */
 int ltk_fluid_buffers(const ltk_fluid *e, double **f, double **g, double **phi, double **mu);
 int ltk_fluid_set_params(ltk_fluid *e, const ltk_fluid_params *p);
 /* The engine's CUDA stream (all engine work is ordered on it). */
