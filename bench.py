@@ -44,21 +44,30 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 #: algorithmic HBM bytes per site update.  k_collide_stream:
-#: read f,g 2*19*8 + mu 8, write f,g 2*19*8.  k_cs_phi (fused, default) adds the
+#: read f,g 2*19*8 + mu 8, write f,g 2*19*8.  k_cs_phi (fused, opt-in) adds the
 #: next state's phi write (8); its re-read of g' is served by L2, not HBM.
 CS_BYTES_PER_SITE = 616
 CSPHI_BYTES_PER_SITE = 624
 #: whole step, three kernels: phi (read g 152 + write 8) + mu (read 8 + write 8) + 616
 STEP_BYTES_PER_SITE = 792
 PHI_BYTES_PER_SITE, MU_BYTES_PER_SITE = 160, 16
+#: per force form: (collide-stream, mu pass) bytes.  passive: no mu read, no mu pass;
+#: binary-stress: the mu pass also writes p_iso and grad phi (32), which the
+#: collision reads (32).
+FORM_BYTES = {"binary": (616, 16), "passive": (608, 0), "binary-stress": (648, 48)}
 
 
-def step_bytes_per_site(fused: bool, nzl: int) -> float:
+def cs_bytes_per_site(fused: bool, physics: str = "binary") -> int:
+    return CSPHI_BYTES_PER_SITE if fused else FORM_BYTES[physics][0]
+
+
+def step_bytes_per_site(fused: bool, nzl: int, physics: str = "binary") -> float:
     """Algorithmic bytes of one step per site: fused, k_phi runs on the 2
     boundary planes only."""
+    cs, mu = FORM_BYTES[physics]
     if not fused:
-        return STEP_BYTES_PER_SITE
-    return CSPHI_BYTES_PER_SITE + MU_BYTES_PER_SITE + PHI_BYTES_PER_SITE * 2.0 / nzl
+        return PHI_BYTES_PER_SITE + mu + cs
+    return CSPHI_BYTES_PER_SITE + mu + PHI_BYTES_PER_SITE * 2.0 / nzl
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -391,9 +400,10 @@ def run_ours(args, rank, world, local):
     cs_ms = prof[2] / args.steps
     peak, peak_src = measured_hbm_peak()
     kname = "k_cs_phi" if fused else "k_collide_stream"
-    cs_bytes = CSPHI_BYTES_PER_SITE if fused else CS_BYTES_PER_SITE
+    cs_bytes = cs_bytes_per_site(fused, args.physics)
     achieved = cs_bytes * sites_rank / (cs_ms * 1e-3) / 1e9
-    traffic = ncu_traffic(args.shape, args.mode, world, kname)
+    # the committed ncu capture is of the binary form
+    traffic = ncu_traffic(args.shape, args.mode, world, kname) if args.physics == "binary" else None
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved,
                 "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peak_src,
@@ -402,8 +412,8 @@ def run_ours(args, rank, world, local):
                 "share_of_step": prof[2] / max(prof[3], 1e-9),
                 "phi_ms_per_step": prof[0] / args.steps,
                 "mu_ms_per_step": prof[1] / args.steps,
-                "step_bytes_per_site": step_bytes_per_site(fused, nzl),
-                "full_step_frac": step_bytes_per_site(fused, nzl) * sites_rank
+                "step_bytes_per_site": step_bytes_per_site(fused, nzl, args.physics),
+                "full_step_frac": step_bytes_per_site(fused, nzl, args.physics) * sites_rank
                 / (ms / args.steps * 1e-3) / 1e9 / peak}
 
     # ---------------- e2e: public API with host buffers, every step
