@@ -179,18 +179,67 @@ class Control:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks, power and throttle reasons sampled during the timed region.
+
+    In-process NVML (nvidia_ml_py) on a thread polling every 2 ms between
+    start() and stop(), so even a 40 ms timed region gets ~20 samples, all
+    inside it; nvidia-smi -lms 20 as the fallback when NVML is unavailable
+    (its ~100 ms start-up makes it sample mostly after short regions)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    #: NVML clocks-event (throttle) reason bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
         self.path = None
+        self.nv = None
+        self.thread = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+            self.nv = pynvml
+        except Exception:
+            self.nv = None
+
+    def _reasons(self):
+        nv = self.nv
+        fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        return int(fn(self.handle))
+
+    def _poll(self):
+        nv, h = self.nv, self.handle
+        while True:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1000.0)
+                self.mask |= self._reasons()
+            except Exception:
+                pass
+            if self.done.wait(0.002):
+                break
 
     def start(self):
+        if self.nv is not None:
+            import threading
+
+            self.sm, self.power, self.mask = [], [], 0
+            try:
+                self.smax = float(self.nv.nvmlDeviceGetMaxClockInfo(self.handle,
+                                                                    self.nv.NVML_CLOCK_SM))
+            except Exception:
+                self.smax = None
+            self.done = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
         try:
             fd, self.path = tempfile.mkstemp(suffix=".csv")
             os.close(fd)
@@ -202,6 +251,15 @@ class ClockSampler:
             self.proc = None
 
     def stop(self) -> dict:
+        if self.thread is not None:
+            self.done.set()
+            self.thread.join()
+            self.thread = None
+            reasons = sorted(k for k, b in self.BITS.items() if self.mask & b)
+            return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                    "sm_max_mhz": self.smax,
+                    "power_w_max": max(self.power) if self.power else None,
+                    "samples": len(self.sm), "reasons": reasons, "source": "nvml, 2 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -230,7 +288,7 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(smax) if smax else None,
                 "power_w_max": max(power) if power else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "reasons": sorted(reasons), "source": "nvidia-smi -lms 20"}
 
 
 def measured_hbm_peak():
