@@ -310,8 +310,8 @@ __device__ __forceinline__ void fsite_finish(FSite &s, double gmx, double gmy, d
 // canonical velocity; the opposite velocity gets -q and sq, which leaves the
 // bracket ((1 + q) + sq) - t bit-identical (see collide.cu relax_exact).
 template <int I, int MODE, int PHYS, int T1>
-__device__ __forceinline__ void frelax(double &f, double &g, double q, double sq, const FSite &s,
-                                       const FluidArgs &a) {
+__device__ __forceinline__ void frelax(double &f, double &g, double q, double sq, double s2,
+                                       const FSite &s, const FluidArgs &a) {
     if constexpr (MODE == LTK_MODE_EXACT) {
         using M = Exact;
         const double br = M::sub(M::add(M::add(1.0, q), sq), s.t);
@@ -322,12 +322,11 @@ __device__ __forceinline__ void frelax(double &f, double &g, double q, double sq
         if constexpr (T1 & 1) fn = M::sub(f, df);
         else fn = M::sub(f, div_rcp(df, a.tau_f, a.inv_tau_f));
         if constexpr (PHYS >= 1) {
-            const double ud = dot_c<cx(I), cy(I), cz(I), M>(s.ux, s.uy, s.uz);
+            // s2 = ((u.c)(F.c))/(cs2 cs2) from the pair (frelax_pair): the opposite
+            // velocity's factors are both negated exactly, so the product is equal
             const double cF = dot_c<cx(I), cy(I), cz(I), M>(s.Fx, s.Fy, s.Fz);
-            const double src =
-                M::mul(M::mul(a.srcpre, a.wv[I]),
-                       M::add(div_rcp(M::sub(cF, s.uF), a.cs2, a.inv_cs2),
-                              div_rcp(M::mul(ud, cF), a.cs2sq, a.inv_cs2sq)));
+            const double src = M::mul(M::mul(a.srcpre, a.wv[I]),
+                                      M::add(div_rcp(M::sub(cF, s.uF), a.cs2, a.inv_cs2), s2));
             fn = M::add(fn, src);
             geq = M::add(geq, M::mul(a.lam[I], s.psi));
         }
@@ -358,15 +357,19 @@ template <int C, int MODE, int PHYS, int T1, int VVL>
 __device__ __forceinline__ void frelax_pair(double (&F)[Q][VVL], double (&G)[Q][VVL], int k,
                                             const FSite &s, const FluidArgs &a) {
     constexpr int O = opp(C);
-    double q = 0.0, sq = 0.0;
+    double q = 0.0, sq = 0.0, s2 = 0.0;
     if constexpr (MODE == LTK_MODE_EXACT) {
         using M = Exact;
         const double ud = dot_c<cx(C), cy(C), cz(C), M>(s.ux, s.uy, s.uz);
         q = div_rcp(ud, a.cs2, a.a1);
         sq = div_rcp(M::mul(ud, ud), a.c2, a.a2);
+        if constexpr (PHYS >= 1) {
+            const double cF = dot_c<cx(C), cy(C), cz(C), M>(s.Fx, s.Fy, s.Fz);
+            s2 = div_rcp(M::mul(ud, cF), a.cs2sq, a.inv_cs2sq);
+        }
     }
-    frelax<C, MODE, PHYS, T1>(F[C][k], G[C][k], q, sq, s, a);
-    if constexpr (O != C) frelax<O, MODE, PHYS, T1>(F[O][k], G[O][k], -q, sq, s, a);
+    frelax<C, MODE, PHYS, T1>(F[C][k], G[C][k], q, sq, s2, s, a);
+    if constexpr (O != C) frelax<O, MODE, PHYS, T1>(F[O][k], G[O][k], -q, sq, s2, s, a);
 }
 
 // One VVL-site chunk of the pull + forced collision.  HINT bit 0: the input
