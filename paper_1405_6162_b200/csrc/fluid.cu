@@ -66,6 +66,7 @@ static void fill_args(FluidArgs &a, const ltk_slab *s, const ltk_fluid_params *p
         a.c2 = a.c1 * p->cs2;
         a.cs2sq = p->cs2 * p->cs2;
         a.srcpre = 1.0 - 0.5 / p->tau_f;
+        for (int i = 0; i < Q; ++i) a.sw[i] = a.srcpre * a.wv[i];
         a.inv_tau_f = 1.0 / p->tau_f;
         a.inv_tau_g = 1.0 / p->tau_g;
         a.a1 = 1.0 / p->cs2;

@@ -61,6 +61,7 @@ struct FluidArgs {
     unsigned ncta_cs, ncta;    // CTAs with collide work / all CTAs
     double wv[Q];
     double lam[Q];
+    double sw[Q];  // srcpre * wv[i] (host, the same RN product the oracle forms per site)
     double cs2, tau_f, tau_g, A, B, kappa, gamma;
     // derived (host-computed once, each the same IEEE expression as the oracle)
     double c1, c2, cs2sq, srcpre;                 // 2cs2, (2cs2)cs2, cs2*cs2, 1 - 0.5/tau_f
@@ -325,7 +326,7 @@ __device__ __forceinline__ void frelax(double &f, double &g, double q, double sq
             // s2 = ((u.c)(F.c))/(cs2 cs2) from the pair (frelax_pair): the opposite
             // velocity's factors are both negated exactly, so the product is equal
             const double cF = dot_c<cx(I), cy(I), cz(I), M>(s.Fx, s.Fy, s.Fz);
-            const double src = M::mul(M::mul(a.srcpre, a.wv[I]),
+            const double src = M::mul(a.sw[I],
                                       M::add(div_rcp(M::sub(cF, s.uF), a.cs2, a.inv_cs2), s2));
             fn = M::add(fn, src);
             geq = M::add(geq, M::mul(a.lam[I], s.psi));
@@ -342,7 +343,7 @@ __device__ __forceinline__ void frelax(double &f, double &g, double q, double sq
         double fn = fma(feq - f, a.inv_tau_f, f);
         if constexpr (PHYS >= 1) {
             const double cF = dot_c<cx(I), cy(I), cz(I), Fast>(s.Fx, s.Fy, s.Fz);
-            const double src = (a.srcpre * a.wv[I]) *
+            const double src = a.sw[I] *
                                fma(ud * cF, a.inv_cs2sq, (cF - s.uF) * a.inv_cs2);
             fn += src;
             geq = fma(a.lam[I], s.psi, geq);
