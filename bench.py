@@ -401,19 +401,44 @@ def run_ours(args, rank, world, local):
     shape = lk.LatticeShape(nx, ny, nzl * world)
     mode = lk.MODE_FAST if args.mode == "fast" else lk.MODE_EXACT
     model = lk.D3Q19Model(tau_f=args.tau, tau_g=args.tau)
-    sim = lk.BinaryFluid(shape, model=model, physics=args.physics, mode=mode, vvl=args.vvl,
-                         rank=rank, nranks=world, device=local, use_graph=False)
     fused = args.fuse
-    sim.set_fuse(fused, args.fuse_lag)
     want = args.layout or ("soa" if fused else "row")
-    sim.set_layout(lk.LAYOUT_ROW if want == "row" else lk.LAYOUT_SOA)
-    if world > 1 and args.transport == "nccl":
+
+    def make_sim():
+        s = lk.BinaryFluid(shape, model=model, physics=args.physics, mode=mode, vvl=args.vvl,
+                           rank=rank, nranks=world, device=local, use_graph=False)
+        s.set_fuse(fused, args.fuse_lag)
+        s.set_layout(lk.LAYOUT_ROW if want == "row" else lk.LAYOUT_SOA)
+        return s
+
+    sim = make_sim()
+    transport = args.transport if world > 1 else "local"
+    if transport == "peer":
+        # collective on every rank: a failed IPC export/mapping anywhere (no P2P
+        # between some pair of GPUs) moves ALL ranks to NCCL instead of failing
+        try:
+            blob = sim.ipc_blob()
+        except Exception as exc:  # noqa: BLE001
+            print(f"warning: rank {rank}: IPC export failed: {exc}", file=sys.stderr)
+            blob = bytes(nat.IPC_BLOB_BYTES)
+        blobs = ctl.allgather_bytes(blob)
+        good = 1.0
+        if all(any(b) for b in blobs):
+            try:
+                sim.attach_peers(blobs[(rank + 1) % world], blobs[(rank - 1) % world])
+            except Exception as exc:  # noqa: BLE001
+                print(f"warning: rank {rank}: peer attach failed: {exc}", file=sys.stderr)
+                good = 0.0
+        else:
+            good = 0.0
+        if ctl.allreduce(good, "MIN") < 1.0:
+            sim.close()
+            sim = make_sim()
+            transport = "nccl (peer transport unavailable)"
+        ctl.barrier()  # every inbox reset before any neighbour primes it
+    if transport.startswith("nccl"):
         uid = lk.nccl_unique_id() if rank == 0 else None
         sim.attach_nccl(ctl.bcast_bytes(uid, 128))
-    elif world > 1:
-        blobs = ctl.allgather_bytes(sim.ipc_blob())
-        sim.attach_peers(blobs[(rank + 1) % world], blobs[(rank - 1) % world])
-        ctl.barrier()  # every inbox reset before any neighbour primes it
     layout = "row" if sim.set_layout(None) == lk.LAYOUT_ROW else "soa"
 
     # per-slab synthetic state in reference order (x*ny + y)*nzl + z
@@ -444,7 +469,7 @@ def run_ours(args, rank, world, local):
     tot1 = [ctl.allreduce(float(v), "SUM") for v in sim.totals()]
     launches = nat.launch_count() - l_before
     # peer transport: a progress wait that ran out of budget means stale halos
-    peer_timeout = bool(world > 1 and args.transport == "peer" and sim.peer_timed_out())
+    peer_timeout = bool(transport == "peer" and sim.peer_timed_out())
     peer_timeout = ctl.allreduce(float(peer_timeout), "MAX") > 0
     ctl.barrier()
     clk = clocks.stop() if rank == 0 else None
@@ -516,7 +541,7 @@ def run_ours(args, rank, world, local):
                              "no flush needed",
                        "parallelism": f"z-slab x{world}",
                        "halo_transport": ("periodic images (one slab)" if world == 1 else
-                                          args.transport)},
+                                          transport)},
             "gpu_launches": launches_all,
             "peer_wait_timeout": peer_timeout,
             "conservation": {"steps": args.warmup + args.steps,
