@@ -558,24 +558,32 @@ class TestStencilKernels:
 
 class TestRandomShapes:
     """Hypothesis-driven parity: random lattice shapes (nx*ny even, the engine's
-    16-byte row rule), physics, tau and step counts, EXACT bitwise vs the oracle."""
+    16-byte row rule; some multiples of 32 x 8 so the register mu kernel runs),
+    physics, tau, step counts, f/g layout and the fused step, EXACT bitwise vs
+    the oracle.  LTK_HYP_EXAMPLES raises the example count (default 30)."""
 
     def test_random_shapes_bitwise(self, lk):
         from hypothesis import given, settings
         from hypothesis import strategies as st
 
-        @settings(max_examples=30, deadline=None)
-        @given(nx=st.integers(1, 12), ny=st.integers(1, 12), nz=st.integers(1, 9),
+        @settings(max_examples=int(os.environ.get("LTK_HYP_EXAMPLES", "30")), deadline=None)
+        @given(nx=st.one_of(st.integers(1, 12), st.sampled_from([32, 64])),
+               ny=st.one_of(st.integers(1, 12), st.sampled_from([8, 16])),
+               nz=st.integers(1, 9),
                physics=st.sampled_from(["passive", "binary", "binary-stress"]),
                tau=st.sampled_from([(1.0, 1.0), (0.8, 1.3), (1.6, 0.7)]),
-               steps=st.integers(1, 3), seed=st.integers(0, 10 ** 6))
-        def check(nx, ny, nz, physics, tau, steps, seed):
+               steps=st.integers(1, 3), seed=st.integers(0, 10 ** 6),
+               row=st.booleans(), fuse=st.booleans())
+        def check(nx, ny, nz, physics, tau, steps, seed, row, fuse):
+            seen.append((nx, ny, nz, physics, row, fuse))
             if (nx * ny) % 2:
                 nx += 1
             shape = (nx, ny, nz)
             f0, g0 = _state(lk, shape, seed)
             model = lk.D3Q19Model(tau_f=tau[0], tau_g=tau[1])
             with lk.BinaryFluid(lk.LatticeShape(*shape), model=model, physics=physics) as sim:
+                sim.set_layout(lk.LAYOUT_ROW if row and nx % 2 == 0 else lk.LAYOUT_SOA)
+                sim.set_fuse(fuse, 1)
                 sim.load(f0, g0)
                 sim.run(steps)
                 f1, g1 = sim.fields()
@@ -584,7 +592,11 @@ class TestRandomShapes:
             assert np.array_equal(f1.data.view(np.uint64), of.view(np.uint64)), shape
             assert np.array_equal(g1.data.view(np.uint64), og.view(np.uint64)), shape
 
+        seen = []
         check()
+        print(f"random-shape parity: {len(seen)} examples, "
+              f"{sum(1 for c in seen if c[0] % 32 == 0 and c[1] % 8 == 0)} on the k_mu_blk path, "
+              f"{sum(1 for c in seen if c[4])} row-blocked, {sum(1 for c in seen if c[5])} fused")
 
 
 class TestRowLayout:
