@@ -169,3 +169,64 @@ def test_two_process_peer_slabs_bitwise(physics, layout):
     ok, timed_out = q.get(timeout=5)
     assert not timed_out
     assert ok
+
+
+def test_engines_in_one_process_random_bitwise():
+    """Hypothesis over the peer transport: slab count, slab depth, plane shape,
+    physics, layout, fused step; the gathered lattice bitwise vs the oracle.
+    LTK_HYP_EXAMPLES raises the example count (default 15)."""
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+
+    import paper_1405_6162_b200 as lk
+    from oracle import oracle as orc
+    from paper_1405_6162_b200.kernels import random_binary_state
+
+    n = int(os.environ.get("LTK_HYP_EXAMPLES", "15"))
+
+    @settings(max_examples=n, deadline=None)
+    @given(nslabs=st.integers(2, 4), nzl=st.integers(2, 6),
+           nx=st.sampled_from([2, 6, 16, 32]), ny=st.sampled_from([1, 3, 8, 16]),
+           physics=st.sampled_from(["passive", "binary", "binary-stress"]),
+           row=st.booleans(), fuse=st.booleans(), steps=st.integers(1, 3),
+           seed=st.integers(0, 10 ** 6))
+    def check(nslabs, nzl, nx, ny, physics, row, fuse, steps, seed):
+        seen.append((nslabs, row, fuse and nzl >= 5))
+        shape = (nx, ny, nslabs * nzl)
+        full = lk.LatticeShape(*shape)
+        model = lk.D3Q19Model(tau_f=0.9, tau_g=1.1)
+        sims = [lk.BinaryFluid(full, model=model, physics=physics, rank=r, nranks=nslabs,
+                               use_graph=False) for r in range(nslabs)]
+        try:
+            for sim in sims:
+                sim.set_layout(lk.LAYOUT_ROW if row else lk.LAYOUT_SOA)
+                sim.set_fuse(fuse and nzl >= 5, 1)
+            for r, sim in enumerate(sims):
+                sim.attach_peer_engines(sims[(r + 1) % nslabs], sims[(r - 1) % nslabs])
+            f0, g0 = random_binary_state(full, np.random.default_rng(seed), model)
+            for sim in sims:
+                sim.load(f0, g0)
+            for _ in range(steps):
+                for sim in sims:
+                    sim.run(1)
+            parts = [sim.fields(slab_only=True) for sim in sims]
+            assert not any(sim.peer_timed_out() for sim in sims)
+        finally:
+            for sim in sims:
+                sim.close()
+        nz = nslabs * nzl
+        got = [np.concatenate([p[k].components()[:, :nx * ny * nzl].reshape(19, nx, ny, nzl)
+                               for p in parts], axis=3) for k in (0, 1)]
+        prm = orc.fluid_params(tau_f=0.9, tau_g=1.1,
+                               physics={"passive": 0, "binary": 1, "binary-stress": 2}[physics])
+        P = f0.descriptor.padded_sites
+        of, og, _, _ = orc.fluid_step(f0.data, g0.data, shape, P, prm, steps=steps)
+        ref = [a.reshape(19, P)[:, :nx * ny * nz].reshape(19, nx, ny, nz) for a in (of, og)]
+        for a, b in zip(got, ref):
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (shape, nslabs, physics)
+
+    seen = []
+    check()
+    print(f"random peer-slab parity: {len(seen)} examples, "
+          f"{sum(1 for c in seen if c[0] >= 3)} with 3-4 slabs, "
+          f"{sum(1 for c in seen if c[1])} row-blocked, {sum(1 for c in seen if c[2])} fused")
