@@ -260,16 +260,19 @@ int ltk_fluid_set_fuse(ltk_fluid *e, int32_t enable, int32_t extra_lag);
 #define LTK_CS_REG 0
 #define LTK_CS_TMA 1
 int ltk_fluid_cs_variant(int32_t variant, int32_t *previous);
-/* Chemical-potential stencil kernel, process-wide: LTK_MU_AUTO = register
- * 2.5-D block kernel k_mu_blk (nx % 32 == 0, ny % 8 == 0; 8 planes of centre
- * loads in flight per thread), else the TMA shared-memory kernel k_mu_tma,
- * else k_mu; LTK_MU_COL = the marching column kernel k_mu_col in k_mu_blk's
- * place; LTK_MU_TMA skips the register kernels; LTK_MU_PLAIN forces k_mu.
+/* Chemical-potential stencil kernel, process-wide.
+ * LTK_MU_AUTO: the 2.5-D tile kernel k_mu_lds where it applies (nx % 32 == 0,
+ *   ny % 8 == 0; an 8-plane phi tile with halos copied into shared memory by
+ *   cp.async), else the TMA shared-memory kernel k_mu_tma, else k_mu.
+ * LTK_MU_COL / LTK_MU_BLK: the register kernels k_mu_col (marching columns) /
+ *   k_mu_blk (batched centre loads) in k_mu_lds's place.
+ * LTK_MU_TMA skips the 2.5-D kernels; LTK_MU_PLAIN forces k_mu.
  * Bitwise identical.  variant < 0 only queries. */
 #define LTK_MU_AUTO 0
 #define LTK_MU_TMA 1
 #define LTK_MU_PLAIN 2
 #define LTK_MU_COL 3
+#define LTK_MU_BLK 4
 int ltk_fluid_mu_variant(int32_t variant, int32_t *previous);
 
 /* f/g storage layout of an engine.  LTK_LAYOUT_SOA: component-major

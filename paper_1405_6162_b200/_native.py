@@ -24,7 +24,7 @@ MODE_EXACT = 0
 MODE_FAST = 1
 CS_REG = 0
 CS_TMA = 1
-MU_AUTO, MU_TMA, MU_PLAIN, MU_COL = 0, 1, 2, 3
+MU_AUTO, MU_TMA, MU_PLAIN, MU_COL, MU_BLK = 0, 1, 2, 3, 4
 LAYOUT_SOA, LAYOUT_ROW = 0, 1
 
 _ERRORS = {1: ConfigError, 2: BoundsError, 3: ShapeError, 4: AllocationError,

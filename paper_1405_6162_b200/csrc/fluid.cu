@@ -99,9 +99,9 @@ static int launch_phi(const FluidArgs &a, int vvl, cudaStream_t st) {
     return LTK_OK;
 }
 
-// mu stencil kernel (process-wide): LTK_MU_AUTO = k_mu_blk where it applies,
-// else k_mu_tma, else k_mu; LTK_MU_COL = k_mu_col in k_mu_blk's place;
-// LTK_MU_TMA skips both register kernels; LTK_MU_PLAIN = k_mu.
+// mu stencil kernel (process-wide): LTK_MU_AUTO = k_mu_lds where it applies,
+// else k_mu_tma, else k_mu; LTK_MU_COL / LTK_MU_BLK = k_mu_col / k_mu_blk in
+// k_mu_lds's place; LTK_MU_TMA skips the 2.5-D kernels; LTK_MU_PLAIN = k_mu.
 static int &mu_variant() {
     static int v = LTK_MU_AUTO;
     return v;
@@ -110,8 +110,16 @@ static int &mu_variant() {
 static int launch_mu(const FluidArgs &a, int vvl, cudaStream_t st) {
     if (a.nthreads <= 0) return LTK_OK;
     const int variant = mu_variant();
-    if ((variant == LTK_MU_AUTO || variant == LTK_MU_COL) && mu_col_ok(a)) {
-        if (variant == LTK_MU_AUTO) {
+    if ((variant == LTK_MU_AUTO || variant == LTK_MU_COL || variant == LTK_MU_BLK) &&
+        mu_col_ok(a)) {
+        if (variant == LTK_MU_AUTO) {  // shared-memory tile filled by cp.async
+            dim3 grid((unsigned)(a.nx / 32), (unsigned)(a.ny / 8),
+                      (unsigned)((a.nplanes + kMuLdsZ - 1) / kMuLdsZ));
+            k_mu_lds<kMuLdsZ><<<grid, dim3(32, 8), 0, st>>>(a);
+            LTK_CHECK_LAUNCH("k_mu_lds");
+            return LTK_OK;
+        }
+        if (variant == LTK_MU_BLK) {
             dim3 grid((unsigned)(a.nx / 32), (unsigned)(a.ny / 8),
                       (unsigned)((a.nplanes + kMuBlkZ - 1) / kMuBlkZ));
             k_mu_blk<kMuBlkZ><<<grid, dim3(32, 8), 0, st>>>(a);
@@ -945,6 +953,7 @@ static int preload_step_kernels() {
     cudaFuncGetAttributes(&fa, k_mu<4>);
     cudaFuncGetAttributes(&fa, k_mu_col<>);
     cudaFuncGetAttributes(&fa, k_mu_blk<kMuBlkZ>);
+    cudaFuncGetAttributes(&fa, k_mu_lds<kMuLdsZ>);
     cudaFuncGetAttributes(&fa, k_mu_tma<4>);
     cudaFuncGetAttributes(&fa, k_mu_tma<2>);
     cudaFuncGetAttributes(&fa, k_plane_copy);
@@ -1581,7 +1590,7 @@ int ltk_fluid_cs_variant(int32_t variant, int32_t *previous) {
 int ltk_fluid_mu_variant(int32_t variant, int32_t *previous) {
     if (previous) *previous = mu_variant();
     if (variant >= 0) {
-        if (variant > LTK_MU_COL) return fail(LTK_ERR_CONFIG, "unknown mu variant %d", variant);
+        if (variant > LTK_MU_BLK) return fail(LTK_ERR_CONFIG, "unknown mu variant %d", variant);
         mu_variant() = variant;
     }
     return LTK_OK;

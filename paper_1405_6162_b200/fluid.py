@@ -33,7 +33,8 @@ MODE_EXACT = nat.MODE_EXACT
 MODE_FAST = nat.MODE_FAST
 CS_REG = nat.CS_REG
 CS_TMA = nat.CS_TMA
-MU_AUTO, MU_TMA, MU_PLAIN, MU_COL = nat.MU_AUTO, nat.MU_TMA, nat.MU_PLAIN, nat.MU_COL
+MU_AUTO, MU_TMA, MU_PLAIN, MU_COL, MU_BLK = (nat.MU_AUTO, nat.MU_TMA, nat.MU_PLAIN,
+                                            nat.MU_COL, nat.MU_BLK)
 LAYOUT_SOA, LAYOUT_ROW = nat.LAYOUT_SOA, nat.LAYOUT_ROW
 #: passive: the reference collision after streaming; binary: free-energy binary
 #: fluid with the force F = -phi grad(mu); binary-stress: the same fluid with the
@@ -337,9 +338,10 @@ def cs_variant(variant: int | None = None) -> int:
 
 
 def mu_variant(variant: int | None = None) -> int:
-    """Chemical-potential stencil kernel of the process: MU_AUTO (register
-    block kernel k_mu_blk where it applies, else TMA, else plain), MU_COL
-    (the marching column kernel instead of k_mu_blk), MU_TMA, MU_PLAIN.
+    """Chemical-potential stencil kernel of the process: MU_AUTO (the 2.5-D
+    shared-memory tile kernel k_mu_lds where it applies, else TMA, else plain),
+    MU_COL / MU_BLK (the register kernels k_mu_col / k_mu_blk instead of
+    k_mu_lds), MU_TMA, MU_PLAIN.
     Returns the previous value; None only queries."""
     prev = ctypes.c_int32(0)
     nat.check(nat.lib.ltk_fluid_mu_variant(-1 if variant is None else int(variant),

@@ -12,7 +12,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 40 --csv --log-file gpurun_out/launches_exact.csv python bench.py --mode exact --steps 4 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 # one --set full capture per hot kernel, summarised on the box (the reports are
 # large; only the dominant kernel's report is kept for source-level reading)
-for k in k_collide_stream k_phi k_mu_blk; do
+for k in k_collide_stream k_phi k_mu_lds; do
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 3 -c 1 -o gpurun_out/prof_$k python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 python scripts/summarize_ncu.py report gpurun_out/prof_$k.ncu-rep gpurun_out/ncu_$k.json > /dev/null 2>&1
 done
@@ -24,5 +24,5 @@ lk.benchmark_run('binary-collision', lk.LatticeShape(128,128,128), 1, iterations
 python scripts/summarize_ncu.py report gpurun_out/prof_k_collide_128.ncu-rep gpurun_out/ncu_k_collide_128.json > /dev/null 2>&1
 python scripts/summarize_ncu.py launches gpurun_out/launches_fast.csv gpurun_out/launches_fast.json > /dev/null 2>&1
 python scripts/summarize_ncu.py launches gpurun_out/launches_exact.csv gpurun_out/launches_exact.json > /dev/null 2>&1
-rm -f gpurun_out/prof_k_phi.ncu-rep gpurun_out/prof_k_mu_blk.ncu-rep gpurun_out/prof_k_collide_128.ncu-rep
+rm -f gpurun_out/prof_k_phi.ncu-rep gpurun_out/prof_k_mu_lds.ncu-rep gpurun_out/prof_k_collide_128.ncu-rep
 ls -la gpurun_out

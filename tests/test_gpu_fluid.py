@@ -506,14 +506,14 @@ class TestFullSizeProperties:
 
 class TestStencilKernels:
     """The C-ABI stencil launchers against the oracle on random phi slabs, for
-    every mu kernel: k_mu_blk / k_mu_col (register 2.5-D blocks / marching
-    columns; nx % 32 == 0, ny % 8 == 0), k_mu_tma (TMA/shared-memory staged rows; ny % rows == 0, nx even) and
+    every mu kernel: k_mu_lds / k_mu_blk / k_mu_col (2.5-D shared-memory tile /
+    register blocks / marching columns; nx % 32 == 0, ny % 8 == 0), k_mu_tma (TMA/shared-memory staged rows; ny % rows == 0, nx even) and
     the plain k_mu; each variant falls through to the next where it does not
     apply."""
 
     @pytest.mark.parametrize("shape", [(256, 16, 37), (32, 8, 16), (2, 8, 5), (512, 24, 3),
                                        (30, 16, 18), (12, 12, 7), (64, 8, 1), (96, 40, 17)])
-    @pytest.mark.parametrize("variant", [0, 1, 2, 3])
+    @pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
     def test_mu_matches_oracle(self, lk, shape, variant):
         prev = lk.mu_variant(variant)
         try:
