@@ -147,8 +147,9 @@ typedef struct {
     double cs2, tau_f, tau_g;
     double A, B, kappa, gamma;
     int32_t physics; /* 0 = passive (reference collision), 1 = free-energy binary fluid
-                      * with F = -phi grad(mu), 2 = same fluid with the momentum-conserving
-                      * force F = -div P (chemical pressure tensor) */
+                      * with the potential force -phi grad(mu), filtered along its own
+                      * axis (orc_potential_force), 2 = same fluid with the
+                      * momentum-conserving force F = -div P (chemical pressure tensor) */
     int32_t pad_;
 } orc_fluid_params;
 
@@ -269,14 +270,61 @@ static void stress_force(const double *piso, const double *const g[3], double ka
     }
 }
 
+/* Potential form of the force (physics 1), F = -phi grad(mu), with each
+ * component smoothed along its own axis by the [1/4, 1/2, 1/4] filter:
+ *   h_a(x) = -(phi(x) * ((mu(x+a) - mu(x-a)) * 0.5)),
+ *   F_a(x) = ((h_a(x-a) + h_a(x+a)) + (h_a(x) + h_a(x))) * 0.25.
+ * Why the filter: on the lattice the momentum mode j_a with
+ * wavenumber pi along a is invariant under streaming (it flips sign) and
+ * under collision (momentum is conserved), so nothing damps it, and the
+ * unfiltered -phi grad(mu) projects onto it wherever phi varies: a flat
+ * interface then grows a checkerboard velocity until it dissolves.  The
+ * filter's transfer function (1 + cos k)/2 vanishes at k = pi, so the force has
+ * no component on those modes; it keeps sum_x F and leaves F = 0 wherever
+ * mu is uniform (the equilibrium).  h is the unfiltered force, F the filtered
+ * one; both are [nsites] arrays per component. */
+void orc_potential_force(const double *phi, const double *mu, double *h[3], double *F[3],
+                         int64_t nx, int64_t ny, int64_t nz)
+{
+#pragma omp parallel for schedule(static)
+    for (int64_t x = 0; x < nx; ++x)
+        for (int64_t y = 0; y < ny; ++y)
+            for (int64_t z = 0; z < nz; ++z) {
+                const int64_t s = site_of(x, y, z, ny, nz);
+                const double gx = (mu[site_of(wrap(x + 1, nx), y, z, ny, nz)] -
+                                   mu[site_of(wrap(x - 1, nx), y, z, ny, nz)]) * 0.5;
+                const double gy = (mu[site_of(x, wrap(y + 1, ny), z, ny, nz)] -
+                                   mu[site_of(x, wrap(y - 1, ny), z, ny, nz)]) * 0.5;
+                const double gz = (mu[site_of(x, y, wrap(z + 1, nz), ny, nz)] -
+                                   mu[site_of(x, y, wrap(z - 1, nz), ny, nz)]) * 0.5;
+                h[0][s] = -(phi[s] * gx);
+                h[1][s] = -(phi[s] * gy);
+                h[2][s] = -(phi[s] * gz);
+            }
+#pragma omp parallel for schedule(static)
+    for (int64_t x = 0; x < nx; ++x)
+        for (int64_t y = 0; y < ny; ++y)
+            for (int64_t z = 0; z < nz; ++z) {
+                const int64_t s = site_of(x, y, z, ny, nz);
+                const int64_t xm = site_of(wrap(x - 1, nx), y, z, ny, nz),
+                              xp = site_of(wrap(x + 1, nx), y, z, ny, nz),
+                              ym = site_of(x, wrap(y - 1, ny), z, ny, nz),
+                              yp = site_of(x, wrap(y + 1, ny), z, ny, nz),
+                              zm = site_of(x, y, wrap(z - 1, nz), ny, nz),
+                              zp = site_of(x, y, wrap(z + 1, nz), ny, nz);
+                F[0][s] = ((h[0][xm] + h[0][xp]) + (h[0][s] + h[0][s])) * 0.25;
+                F[1][s] = ((h[1][ym] + h[1][yp]) + (h[1][s] + h[1][s])) * 0.25;
+                F[2][s] = ((h[2][zm] + h[2][zp]) + (h[2][s] + h[2][s])) * 0.25;
+            }
+}
+
 /* Collision of one streamed site (f_s, g_s hold the 19 pulled values).
  * physics 0: reference collision (kernels.py:96-125 op order).
- * physics 1: Guo-forced f with F = -phi grad(mu) (a, b, c = grad mu); g_eq with
- *            the lam*(gamma mu - phi cs2) term.
- * physics 2: as 1 with the force given directly (a, b, c = F, stress_force).
+ * physics 1, 2: Guo-forced f with the force (Fx, Fy, Fz) (orc_potential_force
+ *            or stress_force); g_eq with the lam*(gamma mu - phi cs2) term.
  * Returns 0, or 1 if rho <= 0 (site left as streamed). */
-static int collide_site(double *fs, double *gs, double mu, double gmx, double gmy,
-                        double gmz, const orc_fluid_params *p)
+static int collide_site(double *fs, double *gs, double mu, double Fx_in, double Fy_in,
+                        double Fz_in, const orc_fluid_params *p)
 {
     double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
     for (int i = 0; i < Q; ++i) {
@@ -293,15 +341,9 @@ static int collide_site(double *fs, double *gs, double mu, double gmx, double gm
     const double cs2 = p->cs2;
     double Fx = 0.0, Fy = 0.0, Fz = 0.0, ux, uy, uz;
     if (p->physics >= 1) {
-        if (p->physics == 1) {
-            Fx = -(phi * gmx);
-            Fy = -(phi * gmy);
-            Fz = -(phi * gmz);
-        } else {
-            Fx = gmx;
-            Fy = gmy;
-            Fz = gmz;
-        }
+        Fx = Fx_in;
+        Fy = Fy_in;
+        Fz = Fz_in;
         ux = (jx + 0.5 * Fx) / rho;
         uy = (jy + 0.5 * Fy) / rho;
         uz = (jz + 0.5 * Fz) / rho;
@@ -335,7 +377,7 @@ static int collide_site(double *fs, double *gs, double mu, double gmx, double gm
 }
 
 /* One full timestep on host-ordered fields: stream (pull) -> phi -> mu ->
- * grad mu -> collide.  f_in/g_in are post-collision states of the previous
+ * force (physics 1: orc_potential_force; 2: stress_force) -> collide.  f_in/g_in are post-collision states of the previous
  * step; f_out/g_out receive the new post-collision state; phi/mu are
  * scratch [nsites] arrays (left holding this step's phi and mu).
  * Returns the first singular real site or -1. */
@@ -351,10 +393,20 @@ int64_t orc_fluid_step(const double *f_in, const double *g_in, double *f_out,
         orc_mu(phi, mu, nx, ny, nz, p->A, p->B, p->kappa);
     else
         memset(mu, 0, sizeof(double) * nsites);
-    double *aux = NULL, *gr[3] = {NULL, NULL, NULL};
-    if (p->physics == 2) {
-        aux = (double *)malloc(sizeof(double) * 4 * (size_t)nsites);
+    /* physics 1: h (3 arrays) and F (3 arrays); physics 2: p_iso, grad phi */
+    double *aux = NULL, *gr[3] = {NULL, NULL, NULL}, *hh[3] = {NULL, NULL, NULL},
+           *FF[3] = {NULL, NULL, NULL};
+    if (p->physics >= 1) {
+        aux = (double *)malloc(sizeof(double) * 6 * (size_t)nsites);
         if (!aux) return -2;
+    }
+    if (p->physics == 1) {
+        for (int k = 0; k < 3; ++k) {
+            hh[k] = aux + k * nsites;
+            FF[k] = aux + (3 + k) * nsites;
+        }
+        orc_potential_force(phi, mu, hh, FF, nx, ny, nz);
+    } else if (p->physics == 2) {
         gr[0] = aux + nsites;
         gr[1] = aux + 2 * nsites;
         gr[2] = aux + 3 * nsites;
@@ -368,26 +420,19 @@ int64_t orc_fluid_step(const double *f_in, const double *g_in, double *f_out,
         for (int64_t y = 0; y < ny; ++y)
             for (int64_t z = 0; z < nz; ++z) {
                 int64_t s = site_of(x, y, z, ny, nz);
-                double gmx = 0.0, gmy = 0.0, gmz = 0.0, m = mu[s];
+                double Fv[3] = {0.0, 0.0, 0.0}, m = mu[s];
                 if (p->physics == 2) {
-                    double F[3];
-                    stress_force(aux, grc, p->kappa, x, y, z, nx, ny, nz, F);
-                    gmx = F[0];
-                    gmy = F[1];
-                    gmz = F[2];
+                    stress_force(aux, grc, p->kappa, x, y, z, nx, ny, nz, Fv);
                 } else if (p->physics == 1) {
-                    gmx = (mu[site_of(wrap(x + 1, nx), y, z, ny, nz)] -
-                           mu[site_of(wrap(x - 1, nx), y, z, ny, nz)]) * 0.5;
-                    gmy = (mu[site_of(x, wrap(y + 1, ny), z, ny, nz)] -
-                           mu[site_of(x, wrap(y - 1, ny), z, ny, nz)]) * 0.5;
-                    gmz = (mu[site_of(x, y, wrap(z + 1, nz), ny, nz)] -
-                           mu[site_of(x, y, wrap(z - 1, nz), ny, nz)]) * 0.5;
+                    Fv[0] = FF[0][s];
+                    Fv[1] = FF[1][s];
+                    Fv[2] = FF[2][s];
                 }
                 for (int i = 0; i < Q; ++i) {
                     fs[i] = f_out[i * padded + s];
                     gs[i] = g_out[i * padded + s];
                 }
-                if (collide_site(fs, gs, m, gmx, gmy, gmz, p)) {
+                if (collide_site(fs, gs, m, Fv[0], Fv[1], Fv[2], p)) {
                     if (s > bad) bad = s;
                     continue;
                 }
