@@ -43,31 +43,24 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-#: algorithmic HBM bytes per site update.  k_collide_stream:
-#: read f,g 2*19*8 + mu 8, write f,g 2*19*8.  k_cs_phi (fused, opt-in) adds the
-#: next state's phi write (8); its re-read of g' is served by L2, not HBM.
-CS_BYTES_PER_SITE = 616
-CSPHI_BYTES_PER_SITE = 624
-#: whole step, three kernels: phi (read g 152 + write 8) + mu (read 8 + write 8) + 616
-STEP_BYTES_PER_SITE = 792
-PHI_BYTES_PER_SITE, MU_BYTES_PER_SITE = 160, 16
-#: per force form: (collide-stream, mu pass) bytes.  passive: no mu read, no mu pass;
-#: binary-stress: the mu pass also writes p_iso and grad phi (32), which the
-#: collision reads (32).
-FORM_BYTES = {"binary": (616, 16), "passive": (608, 0), "binary-stress": (648, 48)}
+#: algorithmic HBM bytes per site update.  k_collide_stream
+#: (binary): read f,g 2*19*8 + phi 8 + mu 8 (the filtered force's stencils are
+#: L1/L2 hits), write f,g 2*19*8.  k_phi: read g 152 + write phi 8.  k_mu: read
+#: phi 8 + write mu 8.
+PHI_BYTES_PER_SITE = 160
+#: per force form: (collide-stream, mu pass) bytes.  passive: no phi/mu read, no
+#: mu pass; binary-stress: the mu pass also writes p_iso and grad phi (32), which
+#: the collision reads (32) instead of phi.
+FORM_BYTES = {"binary": (624, 16), "passive": (608, 0), "binary-stress": (648, 48)}
 
 
-def cs_bytes_per_site(fused: bool, physics: str = "binary") -> int:
-    return CSPHI_BYTES_PER_SITE if fused else FORM_BYTES[physics][0]
+def cs_bytes_per_site(physics: str = "binary") -> int:
+    return FORM_BYTES[physics][0]
 
 
-def step_bytes_per_site(fused: bool, nzl: int, physics: str = "binary") -> float:
-    """Algorithmic bytes of one step per site: fused, k_phi runs on the 2
-    boundary planes only."""
+def step_bytes_per_site(physics: str = "binary") -> int:
     cs, mu = FORM_BYTES[physics]
-    if not fused:
-        return PHI_BYTES_PER_SITE + mu + cs
-    return CSPHI_BYTES_PER_SITE + mu + PHI_BYTES_PER_SITE * 2.0 / nzl
+    return PHI_BYTES_PER_SITE + mu + cs
 FALLBACK_HBM_GBS = 6650.0
 
 
@@ -88,8 +81,8 @@ def parse_args(argv=None):
                         "FMA/reciprocal arithmetic within 1e-12")
     p.add_argument("--vvl", type=int, default=1)
     p.add_argument("--physics", choices=("binary", "binary-stress", "passive"), default="binary",
-                   help="force form: -phi grad mu (default, north star), the momentum-conserving "
-                        "stress divergence, or none")
+                   help="force form: the filtered potential form -phi grad mu (default, north "
+                        "star), the momentum-conserving stress divergence, or none")
     p.add_argument("--tau", type=float, default=1.0,
                    help="tau_f = tau_g (reference default 1.0, model.py:48-49)")
     p.add_argument("--e2e-steps", type=int, default=48,
@@ -100,16 +93,10 @@ def parse_args(argv=None):
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--seed", type=int, default=1234)
-    p.add_argument("--fuse", action="store_true",
-                   help="k_cs_phi (collide-stream + next-state phi) instead of the "
-                        "three-kernel step")
-    p.add_argument("--fuse-lag", type=int, default=1,
-                   help="planes of slack between the collision and phi fronts of k_cs_phi")
-    p.add_argument("--layout", choices=("soa", "row"), default=None,
+    p.add_argument("--layout", choices=("soa", "row"), default="row",
                    help="f/g storage: component-major planes (soa) or row-blocked (row: "
-                        "the 19 components of an x-row adjacent); bitwise identical. "
-                        "The NCCL transport always uses soa; default row, soa with --fuse "
-                        "(measured faster for each)")
+                        "the 19 components of an x-row adjacent; default, measured faster); "
+                        "bitwise identical, every transport takes either")
     p.add_argument("--transport", choices=("peer", "nccl"), default="peer",
                    help="N>1 halo exchange: peer stores from the kernels (CUDA IPC over "
                         "NVLink) or NCCL send/recv")
@@ -401,14 +388,12 @@ def run_ours(args, rank, world, local):
     shape = lk.LatticeShape(nx, ny, nzl * world)
     mode = lk.MODE_FAST if args.mode == "fast" else lk.MODE_EXACT
     model = lk.D3Q19Model(tau_f=args.tau, tau_g=args.tau)
-    fused = args.fuse
-    want = args.layout or ("soa" if fused else "row")
+    want = args.layout
 
     def make_sim():
         s = lk.BinaryFluid(shape, model=model, physics=args.physics, mode=mode, vvl=args.vvl,
                            rank=rank, nranks=world, device=local, use_graph=False)
-        s.set_fuse(fused, args.fuse_lag)
-        s.set_layout(lk.LAYOUT_ROW if want == "row" else lk.LAYOUT_SOA)
+        s.set_layout(lk.LAYOUT_ROW if want == "row" and nx % 2 == 0 else lk.LAYOUT_SOA)
         return s
 
     sim = make_sim()
@@ -479,11 +464,11 @@ def run_ours(args, rank, world, local):
     total_sites = sites_rank * world
     value = total_sites * args.steps / (ms_max * 1e-3) / 1e6  # MLUPS
 
-    # dominant kernel: k_cs_phi (fused) or k_collide_stream, all planes -- prof[2] covers it
+    # dominant kernel: k_collide_stream, all planes -- prof[2] covers it
     cs_ms = prof[2] / args.steps
     peak, peak_src = measured_hbm_peak()
-    kname = "k_cs_phi" if fused else "k_collide_stream"
-    cs_bytes = cs_bytes_per_site(fused, args.physics)
+    kname = "k_collide_stream"
+    cs_bytes = cs_bytes_per_site(args.physics)
     achieved = cs_bytes * sites_rank / (cs_ms * 1e-3) / 1e9
     # the committed ncu capture is of the binary form
     traffic = ncu_traffic(args.shape, args.mode, world, kname) if args.physics == "binary" else None
@@ -495,8 +480,8 @@ def run_ours(args, rank, world, local):
                 "share_of_step": prof[2] / max(prof[3], 1e-9),
                 "phi_ms_per_step": prof[0] / args.steps,
                 "mu_ms_per_step": prof[1] / args.steps,
-                "step_bytes_per_site": step_bytes_per_site(fused, nzl, args.physics),
-                "full_step_frac": step_bytes_per_site(fused, nzl, args.physics) * sites_rank
+                "step_bytes_per_site": step_bytes_per_site(args.physics),
+                "full_step_frac": step_bytes_per_site(args.physics) * sites_rank
                 / (ms / args.steps * 1e-3) / 1e9 / peak}
 
     # ---------------- e2e: public API with host buffers, every step
@@ -532,10 +517,10 @@ def run_ours(args, rank, world, local):
                        "lattice": f"{nx}x{ny}x{nzl * world}",
                        "shape_per_gpu": f"{nx}x{ny}x{nzl}",
                        "mode": args.mode, "vvl": args.vvl, "tau": args.tau,
-                       "physics": {"binary": "binary free energy, F = -phi grad mu",
+                       "physics": {"binary": "binary free energy, F = -phi grad mu "
+                                             "(axis-filtered)",
                                    "binary-stress": "binary free energy, F = -div P",
                                    "passive": "passive (reference collision)"}[args.physics],
-                       "fused": fused, "fuse_lag": args.fuse_lag if fused else None,
                        "layout": layout,
                        "l2": f"state {4 * 19 * 8 * nx * ny * nzl / 1e9:.1f} GB/GPU >> 126 MB L2, "
                              "no flush needed",

@@ -33,7 +33,7 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define LTK_ABI_VERSION 1
+#define LTK_ABI_VERSION 2
 #define LTK_Q 19
 
 typedef enum {
@@ -95,9 +95,11 @@ int ltk_event_elapsed(void *start, void *stop, float *ms);
 int ltk_stream_wait_event(void *stream, void *event);
 
 /* syncTarget (execution.py:271-281): synchronise `stream`, then read and
- * clear the device error word.  Returns LTK_ERR_SINGULAR (and the lowest
- * offending real site in *site) when a kernel met rho <= 0 at a real
- * lattice site (kernels.py:106-108), else LTK_OK with *site = -1. */
+ * clear the stream's error word (every stream has its own, so kernels of one
+ * TargetDevice never report to another sharing the GPU).  Returns
+ * LTK_ERR_SINGULAR (and the lowest offending real site in *site) when a
+ * kernel launched on `stream` met rho <= 0 at a real lattice site
+ * (kernels.py:106-108), else LTK_OK with *site = -1. */
 int ltk_sync(void *stream, int64_t *site);
 
 /* Kernels launched by this library since load (for the bench's
@@ -156,6 +158,9 @@ int ltk_unpack_sites(double *dst, const double *packed, const int64_t *idx, int6
  * doubles; inside a component, storage plane zs = z + 1 (z = 0..nzl-1 owned,
  * zs = 0 and zs = nzl+1 are halo planes), site (x, y) at zs*nx*ny + y*nx + x
  * (x fastest).  Periodic in x and y; z neighbours come from the halo planes.
+ * phi arrays: (nzl+2)*nx*ny doubles, plane zs = z + 1 (one halo per face).
+ * mu arrays: (nzl+4)*nx*ny doubles, plane zs = z + 2 (two halos per face:
+ * the filtered potential force reads mu at z +- 2).
  */
 typedef struct {
     double wv[LTK_Q];
@@ -163,8 +168,10 @@ typedef struct {
     double cs2, tau_f, tau_g;
     double A, B, kappa, gamma; /* mu = A phi + B phi^3 - kappa lap(phi); mobility gamma */
     int32_t physics;    /* 0 = passive (reference collision), 1 = free-energy binary fluid
-                         * with F = -phi grad(mu), 2 = same with the momentum-conserving
-                         * F = -div P (chemical pressure tensor; engine only) */
+                         * with the potential force -phi grad(mu), each component
+                         * filtered [1/4 1/2 1/4] along its own axis,
+                         * 2 = same with the momentum-conserving F = -div P
+                         * (chemical pressure tensor; engine only) */
     int32_t mode;       /* ltk_mode */
 } ltk_fluid_params;
 
@@ -176,16 +183,21 @@ typedef struct {
 /* phi(x) = sum_i g_i(x - c_i) on owned planes [z_lo, z_hi) (pull). */
 int ltk_fluid_phi(const ltk_slab *s, const double *g, double *phi, int64_t z_lo,
                   int64_t z_hi, void *stream);
-/* mu = A phi + B phi^3 - kappa lap7(phi) on owned planes [z_lo, z_hi). */
+/* mu = A phi + B phi^3 - kappa lap7(phi) on owned planes [z_lo, z_hi);
+ * phi needs its halo planes, mu is written in the two-halo mu layout. */
 int ltk_fluid_mu(const ltk_slab *s, const double *phi, double *mu,
                  const ltk_fluid_params *p, int64_t z_lo, int64_t z_hi, void *stream);
-/* Pull-stream + collide owned planes [z_lo, z_hi): f_out(x) = C(f_in(x-c_i), ...). */
+/* Pull-stream + collide owned planes [z_lo, z_hi): f_out(x) = C(f_in(x-c_i), ...).
+ * physics 1 reads phi (x, x+-1 per axis) and mu (x, x+-1, x+-2 per axis);
+ * physics 0 ignores phi/mu; physics 2 runs in the engine only.  rho <= 0
+ * sets the error word of `stream` (ltk_sync). */
 int ltk_fluid_collide_stream(const ltk_slab *s, const double *f_in, const double *g_in,
-                             const double *mu, double *f_out, double *g_out,
-                             const ltk_fluid_params *p, int64_t z_lo, int64_t z_hi,
-                             int32_t vvl, void *stream);
+                             const double *phi, const double *mu, double *f_out,
+                             double *g_out, const ltk_fluid_params *p, int64_t z_lo,
+                             int64_t z_hi, int32_t vvl, void *stream);
 /* Periodic z wrap on one device: copy owned boundary planes into the halo
- * planes.  which: bit0 = f/g crossing components, bit1 = phi, bit2 = mu. */
+ * planes.  which: bit0 = f/g crossing components, bit1 = phi (1 plane per
+ * face), bit2 = mu (2 planes per face). */
 int ltk_fluid_wrap_halos(const ltk_slab *s, double *f, double *g, double *phi, double *mu,
                          int32_t which, void *stream);
 /* Halo faces of the distributions: pack the 5 f + 5 g components that cross
@@ -242,37 +254,23 @@ int ltk_fluid_store(ltk_fluid *e, double *f_dst, double *g_dst, int64_t padded,
  * out5 = {sum rho, sum j_x, sum j_y, sum j_z, sum phi} (synchronous;
  * deterministic block-tree order; sum over slabs for the whole lattice). */
 int ltk_fluid_totals(ltk_fluid *e, double *out5);
-/* Run n full timesteps on the engine stream (or `stream` if not NULL). */
+/* Run n full timesteps on the engine stream (or `stream` if not NULL).
+ * Asynchronous; errors surface at ltk_fluid_sync. */
 int ltk_fluid_run(ltk_fluid *e, int64_t nsteps, void *stream);
+/* syncTarget for an engine: wait for its streams, then read and clear its
+ * own error words.  LTK_ERR_SINGULAR (+ lowest site in host order) when a
+ * kernel met rho <= 0; LTK_ERR_DEVICE when a peer progress wait timed out
+ * (a neighbour stalled: halos are stale, and the engine refuses further
+ * loads and steps). */
+int ltk_fluid_sync(ltk_fluid *e, int64_t *site);
 /* Capture one step pair (A->B, B->A) into CUDA graphs used by ltk_fluid_run. */
 int ltk_fluid_use_graph(ltk_fluid *e, int32_t enable);
-/* Fused collide-stream + next-state phi (k_cs_phi; default off, env
- * LTK_FUSE=1 turns it on): the collide-stream kernel also forms phi of the
- * state it writes, re-reading g' from L2 `extra_lag` + 3 planes behind the
- * collision front, so the next step's k_phi runs on the boundary planes only.
- * Bitwise identical to the three-kernel step. */
-int ltk_fluid_set_fuse(ltk_fluid *e, int32_t enable, int32_t extra_lag);
-/* Collide-stream kernel variant, process-wide: LTK_CS_REG = register-resident
- * loads (k_collide_stream), LTK_CS_TMA = state rows staged in shared memory by
- * TMA bulk copies in a warp-specialised persistent kernel (k_cs_tma; nx a
- * multiple of 128, VVL 1, else the register kernel).  Bitwise identical.
+/* Chemical-potential stencil kernel, process-wide.  LTK_MU_AUTO: the
+ * shared-memory tile kernel k_mu_tile where it applies (nx % 32 == 0,
+ * ny % 8 == 0), else k_mu; LTK_MU_PLAIN forces k_mu.  Bitwise identical.
  * variant < 0 only queries; *previous (if not NULL) gets the old value. */
-#define LTK_CS_REG 0
-#define LTK_CS_TMA 1
-int ltk_fluid_cs_variant(int32_t variant, int32_t *previous);
-/* Chemical-potential stencil kernel, process-wide.
- * LTK_MU_AUTO: the 2.5-D tile kernel k_mu_lds where it applies (nx % 32 == 0,
- *   ny % 8 == 0; an 8-plane phi tile with halos copied into shared memory by
- *   cp.async), else the TMA shared-memory kernel k_mu_tma, else k_mu.
- * LTK_MU_COL / LTK_MU_BLK: the register kernels k_mu_col (marching columns) /
- *   k_mu_blk (batched centre loads) in k_mu_lds's place.
- * LTK_MU_TMA skips the 2.5-D kernels; LTK_MU_PLAIN forces k_mu.
- * Bitwise identical.  variant < 0 only queries. */
 #define LTK_MU_AUTO 0
-#define LTK_MU_TMA 1
-#define LTK_MU_PLAIN 2
-#define LTK_MU_COL 3
-#define LTK_MU_BLK 4
+#define LTK_MU_PLAIN 1
 int ltk_fluid_mu_variant(int32_t variant, int32_t *previous);
 
 /* f/g storage layout of an engine.  LTK_LAYOUT_SOA: component-major
@@ -283,8 +281,8 @@ int ltk_fluid_mu_variant(int32_t variant, int32_t *previous);
  * measured ~1.5% faster on the full step).  Results are bitwise identical; only the
  * engine's own buffers change (ltk_fluid_buffers' f/g pointers then hold
  * that layout).  Set before ltk_fluid_load and before attaching a transport
- * (the state is undefined after a change); ltk_fluid_attach_nccl switches the
- * slab to SoA (NCCL sends contiguous planes); peer slabs must agree.  The
+ * (the state is undefined after a change); every transport works with
+ * either layout (NCCL faces are packed); peer slabs must agree.  The
  * environment variable LTK_LAYOUT=0 makes SoA the default of new engines.  layout < 0 only queries (*previous).  Not in the reference: a
  * B200 layout choice. */
 #define LTK_LAYOUT_SOA 0
@@ -300,14 +298,17 @@ int ltk_fluid_profile(ltk_fluid *e, int32_t enable, float *ms4);
  * buffers (peer stores over NVLink) and progress counters pushed into the
  * neighbours' inboxes order the phases -- the halo exchange is fused into the
  * producing kernels.  Call before ltk_fluid_load. */
-#define LTK_IPC_BLOB_BYTES 512
+#define LTK_IPC_BLOB_BYTES 1024
 int ltk_fluid_ipc_blob(ltk_fluid *e, char *blob);
 int ltk_fluid_attach_peers(ltk_fluid *e, const char *up_blob, const char *dn_blob);
 /* Same transport between engines of one process (one thread driving several
  * GPUs, or several slabs on one GPU): peers given directly. */
 int ltk_fluid_attach_peer_engines(ltk_fluid *e, const ltk_fluid *up, const ltk_fluid *dn);
-/* 1 if a peer progress wait ever exceeded its budget (never expected). */
+/* 1 if a peer progress wait ever exceeded its budget (~8 s; never expected). */
 int ltk_fluid_peer_timeout(ltk_fluid *e, int32_t *timed_out);
+/* Test hook: the engine's next progress waits fail at once, as if a
+ * neighbour had stalled. */
+int ltk_fluid_inject_peer_timeout(ltk_fluid *e);
 
 /* NCCL (dlopen'ed libnccl.so.2): the 128-byte unique id of rank 0 is
  * broadcast by the caller (torch.distributed) before attach. */

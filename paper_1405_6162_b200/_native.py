@@ -18,13 +18,12 @@ LIB_PATH = os.path.join(HERE, "_native", "libltk.so")
 Q = 19
 
 LTK_OK = 0
-IPC_BLOB_BYTES = 512
+IPC_BLOB_BYTES = 1024
+ABI_VERSION = 2
 LTK_ERR_SINGULAR = 11
 MODE_EXACT = 0
 MODE_FAST = 1
-CS_REG = 0
-CS_TMA = 1
-MU_AUTO, MU_TMA, MU_PLAIN, MU_COL, MU_BLK = 0, 1, 2, 3, 4
+MU_AUTO, MU_PLAIN = 0, 1
 LAYOUT_SOA, LAYOUT_ROW = 0, 1
 
 _ERRORS = {1: ConfigError, 2: BoundsError, 3: ShapeError, 4: AllocationError,
@@ -99,8 +98,8 @@ SIGNATURES = {
     "ltk_fluid_mu": (ctypes.c_int, [ctypes.POINTER(Slab), _vp, _vp, ctypes.POINTER(FluidParams),
                                     _i64, _i64, _vp]),
     "ltk_fluid_collide_stream": (ctypes.c_int, [ctypes.POINTER(Slab), _vp, _vp, _vp, _vp, _vp,
-                                                ctypes.POINTER(FluidParams), _i64, _i64, _i32,
-                                                _vp]),
+                                                _vp, ctypes.POINTER(FluidParams), _i64, _i64,
+                                                _i32, _vp]),
     "ltk_fluid_wrap_halos": (ctypes.c_int, [ctypes.POINTER(Slab), _vp, _vp, _vp, _vp, _i32,
                                             _vp]),
     "ltk_fluid_pack_face": (ctypes.c_int, [ctypes.POINTER(Slab), _vp, _vp, _vp, _i32, _vp]),
@@ -121,8 +120,7 @@ SIGNATURES = {
     "ltk_fluid_run": (ctypes.c_int, [_vp, _i64, _vp]),
     "ltk_fluid_totals": (ctypes.c_int, [_vp, ctypes.POINTER(_dbl)]),
     "ltk_fluid_use_graph": (ctypes.c_int, [_vp, _i32]),
-    "ltk_fluid_set_fuse": (ctypes.c_int, [_vp, _i32, _i32]),
-    "ltk_fluid_cs_variant": (ctypes.c_int, [_i32, ctypes.POINTER(_i32)]),
+    "ltk_fluid_sync": (ctypes.c_int, [_vp, ctypes.POINTER(_i64)]),
     "ltk_div_selftest": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
     "ltk_fluid_mu_variant": (ctypes.c_int, [_i32, ctypes.POINTER(_i32)]),
     "ltk_fluid_set_layout": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(_i32)]),
@@ -131,6 +129,7 @@ SIGNATURES = {
     "ltk_fluid_attach_peers": (ctypes.c_int, [_vp, ctypes.c_char_p, ctypes.c_char_p]),
     "ltk_fluid_attach_peer_engines": (ctypes.c_int, [_vp, _vp, _vp]),
     "ltk_fluid_peer_timeout": (ctypes.c_int, [_vp, ctypes.POINTER(_i32)]),
+    "ltk_fluid_inject_peer_timeout": (ctypes.c_int, [_vp]),
     "ltk_nccl_available": (ctypes.c_int, []),
     "ltk_nccl_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
     "ltk_fluid_attach_nccl": (ctypes.c_int, [_vp, ctypes.c_char_p]),
@@ -154,6 +153,8 @@ def _load() -> ctypes.CDLL:
         fn.argtypes = args
     if missing:
         raise ImportError(f"libltk.so lacks symbols {missing}: rebuild it")
+    if lib.ltk_abi_version() != ABI_VERSION:
+        raise ImportError(f"libltk.so ABI {lib.ltk_abi_version()} != {ABI_VERSION}: rebuild it")
     return lib
 
 

@@ -244,8 +244,9 @@ extern "C" int ltk_collide(int64_t chunk_lo, int64_t chunk_hi, int32_t vvl, int3
     a.nsites = nsites;
     a.site_lo = chunk_lo * vvl;
     a.nchunks = chunk_hi - chunk_lo;
-    a.err = singular_word();
-    if (!a.err) return fail(LTK_ERR_DEVICE, "device error word unavailable");
+    cudaStream_t st = as_stream(stream);
+    a.err = stream_word(st);
+    if (!a.err) return fail(LTK_ERR_DEVICE, "stream error word unavailable");
     for (int i = 0; i < Q; ++i) a.wv[i] = p->wv[i];
     a.cs2 = p->cs2;
     a.tau_f = p->tau_f;
@@ -257,7 +258,6 @@ extern "C" int ltk_collide(int64_t chunk_lo, int64_t chunk_hi, int32_t vvl, int3
     a.a1 = 1.0 / p->cs2;
     a.a2 = 1.0 / a.c2;
     a.a3 = 1.0 / a.c1;
-    cudaStream_t st = as_stream(stream);
     if (p->mode == LTK_MODE_EXACT) {
         // x / 1.0 == x for every IEEE double: when tau is exactly 1 (the
         // reference default, model.py:48-49) the division is skipped, bitwise neutral

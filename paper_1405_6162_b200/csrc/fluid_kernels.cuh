@@ -1,26 +1,25 @@
 // fluid_kernels.cuh -- device kernels of the full D3Q19 binary-fluid timestep
 // (builder-defined extension).
 //
-// Slab layout: SoA, component stride cstride; storage plane
-// zs = z + 1 holds owned plane z (zs = 0 and nzl + 1 are halo planes); site
-// (x, y, zs) at zs*PL + y*nx + x with PL = nx*ny.  x is fastest, so a z-plane
-// is one contiguous run of PL doubles per component (halo faces are plain
-// contiguous NCCL buffers) and a warp touches 32 consecutive x.
+// Slab layout: x fastest, z slowest.  f/g element (component
+// i, storage plane zs, row y, x) at i*SI + zs*SZ + y*SY + x, storage plane
+// zs = z + 1 (halo planes zs = 0 and nzl + 1); SoA (SI, SZ, SY) =
+// (cstride, nx*ny, nx) or row-blocked (nx, ny*19*nx, 19*nx).  phi planes are
+// plane-major with one halo plane per side (zs = z + 1, nzl + 2 planes); mu
+// (and the stress form's aux arrays) with two (zs = z + 2, nzl + 4 planes),
+// because the filtered potential force reads mu at z +- 2.
 //
 // One timestep = k_phi -> k_mu -> k_collide_stream (pull scheme):
-//   k_phi   phi(x) = sum_i g_i(x - c_i)                         [g pulled]
-//   k_mu    mu = A phi + B phi^3 - kappa lap7(phi)               [phi stencil]
-//   k_cs    pull f, g; phi again in registers; grad mu (central);
-//           Guo-forced BGK for f, chemical-potential g_eq; aligned store.
-// Halo images: a kernel that produces an owned boundary plane also stores it
-// (phi, mu: the plane; f, g: the components that cross the face) straight into
-// the halo plane that needs it -- the top plane into the bottom halo (zs = 0)
-// of the slab above, the bottom plane into the top halo (zs = nzl+1) of the
-// slab below.  One GPU, periodic z: both targets are this slab's own buffers,
-// so a step needs no halo kernels.  z-slabs over NVLink (peer transport): the
-// targets are the neighbours' buffers mapped with CUDA IPC, so the halo
-// exchange is fused into the producing kernels as peer stores.  NCCL
-// transport: no images (null targets); the engine exchanges faces instead.
+//   k_phi   phi(x) = sum_i g_i(x - c_i)                        [g pulled]
+//   k_mu    mu = A phi + B phi^3 - kappa lap7(phi)              [phi stencil]
+//   k_cs    pull f, g; force from the phi / mu stencils; Guo-forced BGK for
+//           f, chemical-potential g_eq; aligned store.
+// Halo images: a kernel that produces an owned plane some other plane's
+// stencil needs across a slab face also stores it straight into the halo
+// plane that needs it -- into this slab's own halos on one GPU (periodic z,
+// no halo kernels), into the neighbours' buffers mapped with CUDA IPC with
+// the peer transport (the halo exchange fused into the producing kernels as
+// NVLink stores), nowhere with NCCL (the engine exchanges faces).
 #pragma once
 
 #include "ltk_common.cuh"
@@ -28,44 +27,34 @@
 namespace ltk {
 
 struct FluidArgs {
-    const double *f_in;
-    const double *g_in;
-    const double *mu;
-    const double *phi_in;
-    double *f_out;
-    double *g_out;
-    double *phi_out;
-    double *mu_out;
-    double *phi_next;  // k_cs_phi: phi of the state being written
-    // physics 2 (stress form): p_iso, d_x phi, d_y phi, d_z phi, slab layout like
-    // mu, at aux + k * astride; written by the mu kernels, read by collide-stream
-    double *aux, *img_aux_up, *img_aux_dn;
+    const double *f_in, *g_in;  // state read (post-collision of the last step)
+    double *f_out, *g_out;      // state written
+    const double *phi;          // phi slab read by k_mu / k_collide_stream
+    double *phi_out;            // phi slab written by k_phi
+    const double *mu;           // mu slab read by k_collide_stream
+    double *mu_out;             // mu slab written by k_mu
+    // physics 2 (stress form): p_iso, d_x phi, d_y phi, d_z phi in mu's layout
+    // at aux + k * astride (after mu in mu's allocation); written by k_mu
+    double *aux;
     long long astride;
-    long long *err;
+    long long *err;  // the engine's / stream's error word (flag_singular)
     int nx, ny, nzl, z_lo, nplanes;
+    int wrap_local;  // images into this slab's own halos (periodic z, one slab)
     // halo image targets (nullptr = none): buffers of the slab above (up) /
-    // below (dn); f/g point at the state being written (f_out/g_out side)
+    // below (dn); f/g point at the state being written; aux images follow mu's
     double *img_f_up, *img_g_up, *img_f_dn, *img_g_dn;
     double *img_phi_up, *img_phi_dn, *img_mu_up, *img_mu_dn;
-    long long PL, cstride;
-    // f/g element (component i, storage plane zs, row y, x) at i*SI + zs*SZ + y*SY + x:
-    // SoA (SI, SZ, SY) = (cstride, PL, nx); row-blocked (nx, ny*Q*nx, Q*nx)
+    long long PL;
     long long SI, SZ, SY;
-    long long nthreads;   // threads of this launch
+    long long nthreads;       // threads of this launch
     long long nz_global, z0;  // for error-site reporting in host order
-    // fused collide-stream + next-state phi (k_cs_phi); see that kernel
-    unsigned long long *sync;  // [0] ticket, [1 + z] plane z sites done (cumulative)
-    long long tpp;             // threads per plane (ny * nx / VVL)
-    int phi_lo, phi_hi;        // phi planes of the next state formed in-kernel
-    unsigned lag_ctas;         // phi work of CTA b is the phi thread range of CTA b - lag_ctas
-    unsigned ncta_cs, ncta;    // CTAs with collide work / all CTAs
     double wv[Q];
     double lam[Q];
     double sw[Q];  // srcpre * wv[i] (host, the same RN product the oracle forms per site)
     double cs2, tau_f, tau_g, A, B, kappa, gamma;
     // derived (host-computed once, each the same IEEE expression as the oracle)
-    double c1, c2, cs2sq, srcpre;                 // 2cs2, (2cs2)cs2, cs2*cs2, 1 - 0.5/tau_f
-    double inv_tau_f, inv_tau_g, a1, a2, a3, inv_cs2, inv_cs2sq;  // FAST
+    double c1, c2, cs2sq, srcpre;                                 // 2cs2, (2cs2)cs2, cs2*cs2, 1 - 0.5/tau_f
+    double inv_tau_f, inv_tau_g, a1, a2, a3, inv_cs2, inv_cs2sq;  // reciprocals
 };
 
 // thread -> (x0, y, z) of a VVL-site row segment
@@ -74,69 +63,55 @@ struct Pos {
 };
 
 template <int VVL>
-__device__ __forceinline__ void pos_of(const FluidArgs &a, unsigned tt, int z_lo, Pos &p) {
+__device__ __forceinline__ bool thread_pos(const FluidArgs &a, Pos &p) {
+    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.nthreads) return false;
+    const unsigned tt = (unsigned)t;
     const unsigned nxv = (unsigned)(a.nx / VVL);
     const unsigned row = tt / nxv;
     p.x0 = (int)(tt - row * nxv) * VVL;
     p.y = (int)(row % (unsigned)a.ny);
-    p.z = z_lo + (int)(row / (unsigned)a.ny);
-}
-
-template <int VVL>
-__device__ __forceinline__ bool thread_pos(const FluidArgs &a, Pos &p) {
-    const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= a.nthreads) return false;
-    pos_of<VVL>(a, (unsigned)t, a.z_lo, p);
+    p.z = a.z_lo + (int)(row / (unsigned)a.ny);
     return true;
 }
 
-// Load flavours of pull(): plain read-only (__ldg), read-only with an L2
-// policy (the fused kernel's input state), L2-only with a policy (state
-// written earlier in the same launch).
-enum { kLdg = 0, kLdNc = 1, kLdCg = 2 };
-
 __device__ __forceinline__ int wrapi(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
+// |v| < 2n (offsets of +-2 on extents >= 1)
+__device__ __forceinline__ int wrap2(int v, int n) { return wrapi(wrapi(v, n), n); }
 
 // Pull the VVL values of component I at sites (x0..x0+VVL-1, y, zs) from
 // (x - cx, y - cy, zs - cz).  cx == 0 -> one aligned vector load.
-template <int I, int VVL, int LD = kLdg>
+template <int I, int VVL>
 __device__ __forceinline__ void pull(double (&v)[VVL], const double *base, const FluidArgs &a,
-                                     const Pos &p, uint64_t pol = 0) {
+                                     const Pos &p) {
     const int ys = wrapi(p.y - cy(I), a.ny);
     const double *row = base + (long long)I * a.SI + (long long)(p.z + 1 - cz(I)) * a.SZ +
                         (long long)ys * a.SY;
     if constexpr (cx(I) == 0) {
-        if constexpr (LD == kLdg) load_vec<VVL>(v, row + p.x0);
-        else if constexpr (LD == kLdNc) load_vec_nc<VVL>(v, row + p.x0, pol);
-        else load_vec_cg<VVL>(v, row + p.x0, pol);
+        load_vec<VVL>(v, row + p.x0);
     } else {
 #pragma unroll
-        for (int k = 0; k < VVL; ++k) {
-            const double *q = row + wrapi(p.x0 + k - cx(I), a.nx);
-            if constexpr (LD == kLdg) v[k] = __ldg(q);
-            else if constexpr (LD == kLdNc) v[k] = ld_nc_pol(q, pol);
-            else v[k] = ld_cg_pol(q, pol);
-        }
+        for (int k = 0; k < VVL; ++k) v[k] = __ldg(row + wrapi(p.x0 + k - cx(I), a.nx));
     }
 }
 
 // ------------------------------------------------------------------ phi
-template <int VVL, int LD, bool IMG = true>
-__device__ __forceinline__ void phi_site(const FluidArgs &a, const Pos &p, const double *g,
-                                         double *out, uint64_t pol) {
+template <int VVL>
+__global__ void __launch_bounds__(128) k_phi(const FluidArgs a) {
+    Pos p;
+    if (!thread_pos<VVL>(a, p)) return;
     double phi[VVL];
 #pragma unroll
     for (int k = 0; k < VVL; ++k) phi[k] = 0.0;
     double v[Q][VVL];  // all loads issued before the first add
-    static_for<0, Q>([&](auto I) { pull<I.value, VVL, LD>(v[I.value], g, a, p, pol); });
+    static_for<0, Q>([&](auto I) { pull<I.value, VVL>(v[I.value], a.g_in, a, p); });
     static_for<0, Q>([&](auto I) {
 #pragma unroll
         for (int k = 0; k < VVL; ++k) phi[k] = __dadd_rn(phi[k], v[I.value][k]);
     });
     const long long off = (long long)p.y * a.nx + p.x0;
-    store_vec<VVL>(out + (long long)(p.z + 1) * a.PL + off, phi);
-    if constexpr (!IMG) return;
-    // halo images for the mu stencil of the neighbouring slabs (or this one)
+    store_vec<VVL>(a.phi_out + (long long)(p.z + 1) * a.PL + off, phi);
+    // halo images for the stencils of the neighbouring slabs (or this one)
     bool img = false;
     if (p.z == 0 && a.img_phi_dn) {
         store_vec<VVL>(a.img_phi_dn + (long long)(a.nzl + 1) * a.PL + off, phi);
@@ -149,20 +124,39 @@ __device__ __forceinline__ void phi_site(const FluidArgs &a, const Pos &p, const
     if (img) __threadfence_system();  // peer images visible before the progress signal
 }
 
-template <int VVL>
-__global__ void __launch_bounds__(256) k_phi(const FluidArgs a) {
-    Pos p;
-    if (!thread_pos<VVL>(a, p)) return;
-    phi_site<VVL, kLdg>(a, p, a.g_in, a.phi_out, 0);
+// ------------------------------------------------------------------ mu
+// mu-layout halo planes an owned plane z feeds: the slab above reads our
+// planes nzl-2, nzl-1 as its z = -2, -1 (storage 0, 1); the slab below reads
+// our planes 0, 1 as its z = nzl, nzl+1 (storage nzl+2, nzl+3).  One slab
+// (wrap_local): halo plane hz holds plane hz mod nzl, which also covers nzl = 1.
+__device__ __forceinline__ int modi(int v, int n) { return ((v % n) + n) % n; }
+
+template <class Store>
+__device__ __forceinline__ bool mu_images(const FluidArgs &a, int z, Store store) {
+    bool img = false;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int hz_up = k - 2;       // the slab above's halo plane
+        const int hz_dn = a.nzl + k;   // the slab below's halo plane
+        const int src_up = a.wrap_local ? modi(hz_up, a.nzl) : a.nzl + hz_up;
+        const int src_dn = a.wrap_local ? modi(hz_dn, a.nzl) : k;
+        if (a.img_mu_up && z == src_up) {
+            store(a.img_mu_up, (long long)(hz_up + 2) * a.PL);
+            img = true;
+        }
+        if (a.img_mu_dn && z == src_dn) {
+            store(a.img_mu_dn, (long long)(hz_dn + 2) * a.PL);
+            img = true;
+        }
+    }
+    return img;
 }
 
-// ------------------------------------------------------------------ mu
-// physics 2 side outputs of the mu kernels at storage offset o = zs*PL + off:
-// p_iso and the central gradient of phi (oracle orc_stress op order), plus
-// their halo images for the boundary planes (like mu's).
-__device__ __forceinline__ void stress_store(const FluidArgs &a, int z, long long off, double ph,
-                                             double mu, double xp, double xm, double yp, double ym,
-                                             double zp, double zm) {
+// physics 2 side outputs of the mu kernels: p_iso and the central gradient of
+// phi (oracle orc_stress op order).
+__device__ __forceinline__ void stress_values(const FluidArgs &a, double ph, double mu, double xp,
+                                              double xm, double yp, double ym, double zp,
+                                              double zm, double (&v)[4]) {
     using M = Exact;
     const double gx = M::mul(M::sub(xp, xm), 0.5);
     const double gy = M::mul(M::sub(yp, ym), 0.5);
@@ -170,65 +164,115 @@ __device__ __forceinline__ void stress_store(const FluidArgs &a, int z, long lon
     const double gsq = M::add(M::add(M::mul(gx, gx), M::mul(gy, gy)), M::mul(gz, gz));
     const double pp = M::mul(ph, ph);
     const double fb = M::add(M::mul(M::mul(0.5, a.A), pp), M::mul(M::mul(0.25, a.B), M::mul(pp, pp)));
-    const double piso = M::sub(M::sub(M::mul(ph, mu), fb), M::mul(M::mul(0.5, a.kappa), gsq));
-    const double v[4] = {piso, gx, gy, gz};
-    const long long o = (long long)(z + 1) * a.PL + off;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) a.aux[k * a.astride + o] = v[k];
-    if (z == 0 && a.img_aux_dn) {
-        const long long h = (long long)(a.nzl + 1) * a.PL + off;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) a.img_aux_dn[k * a.astride + h] = v[k];
-    }
-    if (z == a.nzl - 1 && a.img_aux_up) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) a.img_aux_up[k * a.astride + off] = v[k];
-    }
+    v[0] = M::sub(M::sub(M::mul(ph, mu), fb), M::mul(M::mul(0.5, a.kappa), gsq));
+    v[1] = gx;
+    v[2] = gy;
+    v[3] = gz;
 }
 
+// mu of one site from its 7-point phi neighbourhood, stored with the stress
+// outputs and the halo images where they apply (oracle orc_mu op order):
 // mu = (A phi + B phi^3) - kappa lap, lap = (((((phi(x+1) + phi(x-1)) + phi(y+1))
-//      + phi(y-1)) + phi(z+1)) + phi(z-1)) - 6 phi   (oracle orc_mu op order)
+//      + phi(y-1)) + phi(z+1)) + phi(z-1)) - 6 phi.
+__device__ __forceinline__ void mu_site_store(const FluidArgs &a, int z, long long off, double pm,
+                                              double pc, double pp, double vxp, double vxm,
+                                              double vyp, double vym) {
+    double s = __dadd_rn(vxp, vxm);
+    s = __dadd_rn(s, vyp);
+    s = __dadd_rn(s, vym);
+    s = __dadd_rn(s, pp);
+    s = __dadd_rn(s, pm);
+    const double lap = __dsub_rn(s, __dmul_rn(6.0, pc));
+    const double p3 = __dmul_rn(__dmul_rn(pc, pc), pc);
+    const double mu = __dsub_rn(__dadd_rn(__dmul_rn(a.A, pc), __dmul_rn(a.B, p3)),
+                                __dmul_rn(a.kappa, lap));
+    const long long o = (long long)(z + 2) * a.PL + off;
+    a.mu_out[o] = mu;
+    double sv[4];
+    if (a.aux) {
+        stress_values(a, pc, mu, vxp, vxm, vyp, vym, pp, pm, sv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a.aux[k * a.astride + o] = sv[k];
+    }
+    const bool img = mu_images(a, z, [&](double *dst, long long plane) {
+        dst[plane + off] = mu;
+        if (a.aux)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) dst[(k + 1) * a.astride + plane + off] = sv[k];
+    });
+    if (img) __threadfence_system();
+}
+
+// Plain stencil: one thread per VVL sites, neighbours from L1/L2 (any shape).
 template <int VVL>
-__global__ void __launch_bounds__(256) k_mu(const FluidArgs a) {
+__global__ void __launch_bounds__(128) k_mu(const FluidArgs a) {
     Pos p;
     if (!thread_pos<VVL>(a, p)) return;
-    const double *c = a.phi_in + (long long)(p.z + 1) * a.PL;
-    const int yp = wrapi(p.y + 1, a.ny), ym = wrapi(p.y - 1, a.ny);
-    double mu[VVL];
+    const double *c = a.phi + (long long)(p.z + 1) * a.PL;
+    const long long r0 = (long long)p.y * a.nx;
+    const long long rp = (long long)wrapi(p.y + 1, a.ny) * a.nx, rm = (long long)wrapi(p.y - 1, a.ny) * a.nx;
 #pragma unroll
     for (int k = 0; k < VVL; ++k) {
         const int x = p.x0 + k;
-        const int xp = wrapi(x + 1, a.nx), xm = wrapi(x - 1, a.nx);
-        const double ph = __ldg(c + (long long)p.y * a.nx + x);
-        double s = __ldg(c + (long long)p.y * a.nx + xp);
-        s = __dadd_rn(s, __ldg(c + (long long)p.y * a.nx + xm));
-        s = __dadd_rn(s, __ldg(c + (long long)yp * a.nx + x));
-        s = __dadd_rn(s, __ldg(c + (long long)ym * a.nx + x));
-        s = __dadd_rn(s, __ldg(c + a.PL + (long long)p.y * a.nx + x));
-        s = __dadd_rn(s, __ldg(c - a.PL + (long long)p.y * a.nx + x));
-        const double lap = __dsub_rn(s, __dmul_rn(6.0, ph));
-        const double p3 = __dmul_rn(__dmul_rn(ph, ph), ph);
-        mu[k] = __dsub_rn(__dadd_rn(__dmul_rn(a.A, ph), __dmul_rn(a.B, p3)),
-                          __dmul_rn(a.kappa, lap));
-        if (a.aux)
-            stress_store(a, p.z, (long long)p.y * a.nx + x, ph, mu[k],
-                         __ldg(c + (long long)p.y * a.nx + xp), __ldg(c + (long long)p.y * a.nx + xm),
-                         __ldg(c + (long long)yp * a.nx + x), __ldg(c + (long long)ym * a.nx + x),
-                         __ldg(c + a.PL + (long long)p.y * a.nx + x),
-                         __ldg(c - a.PL + (long long)p.y * a.nx + x));
+        mu_site_store(a, p.z, r0 + x, __ldg(c - a.PL + r0 + x), __ldg(c + r0 + x),
+                      __ldg(c + a.PL + r0 + x), __ldg(c + r0 + wrapi(x + 1, a.nx)),
+                      __ldg(c + r0 + wrapi(x - 1, a.nx)), __ldg(c + rp + x), __ldg(c + rm + x));
     }
-    const long long off = (long long)p.y * a.nx + p.x0;
-    store_vec<VVL>(a.mu_out + (long long)(p.z + 1) * a.PL + off, mu);
-    bool img = false;
-    if (p.z == 0 && a.img_mu_dn) {
-        store_vec<VVL>(a.img_mu_dn + (long long)(a.nzl + 1) * a.PL + off, mu);
-        img = true;
+}
+
+// Tile stencil (default where nx % 32 == 0 and ny % 8 == 0): a (32 x 8)
+// column block copies its phi tile -- ZC + 2 planes x 10 rows x 34 columns,
+// halos included -- into shared memory with per-thread cp.async (LDGSTS), so
+// the loads in flight hold no registers, then every neighbour is a
+// shared-memory read.  48 registers, 27 KB: 5 blocks per SM.  Measured
+// (round 1, 256^3): 0.070 ms vs 0.091-0.107 ms for register-resident forms.
+constexpr int kMuTileZ = 8;
+
+inline bool mu_tile_ok(int nx, int ny) { return nx % 32 == 0 && ny % 8 == 0; }
+
+template <int ZC>
+__global__ void __launch_bounds__(256) k_mu_tile(const FluidArgs a) {
+    __shared__ double t[ZC + 2][10][34];
+    const int lane = threadIdx.x, wy = threadIdx.y, nx = a.nx;
+    const int x = blockIdx.x * 32 + lane, y = blockIdx.y * 8 + wy;
+    const int zb = a.z_lo + blockIdx.z * ZC;
+    const int n = min(ZC, a.z_lo + a.nplanes - zb);
+    const long long PL = a.PL;
+    const double *ph = a.phi + (long long)zb * PL;  // storage plane zb = z - 1 of the first
+    const long long r0 = (long long)y * nx;
+    auto cp8 = [](double *dst, const double *src) {
+        const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(src) : "memory");
+    };
+#pragma unroll
+    for (int k = 0; k < ZC + 2; ++k)
+        if (k < n + 2) cp8(&t[k][wy + 1][lane + 1], ph + k * PL + r0 + x);
+    // y halo rows (outer warps) and x halo columns (edge lanes) of the computed planes
+    if (wy == 0 || wy == 7) {
+        const long long rh = (long long)wrapi(wy == 0 ? y - 1 : y + 1, a.ny) * nx;
+        const int row = wy == 0 ? 0 : 9;
+#pragma unroll
+        for (int k = 1; k < ZC + 1; ++k)
+            if (k < n + 1) cp8(&t[k][row][lane + 1], ph + k * PL + rh + x);
     }
-    if (p.z == a.nzl - 1 && a.img_mu_up) {
-        store_vec<VVL>(a.img_mu_up + off, mu);
-        img = true;
+    if (lane == 0 || lane == 31) {
+        const int xh = wrapi(lane == 0 ? x - 1 : x + 1, nx);
+        const int col = lane == 0 ? 0 : 33;
+#pragma unroll
+        for (int k = 1; k < ZC + 1; ++k)
+            if (k < n + 1) cp8(&t[k][wy + 1][col], ph + k * PL + r0 + xh);
     }
-    if (img) __threadfence_system();
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < ZC; ++k) {
+        if (k < n) {
+            const int r = wy + 1, c = lane + 1;
+            mu_site_store(a, zb + k, r0 + x, t[k][r][c], t[k + 1][r][c], t[k + 2][r][c],
+                          t[k + 1][r][c + 1], t[k + 1][r][c - 1], t[k + 1][r + 1][c],
+                          t[k + 1][r - 1][c]);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ collide-stream
@@ -248,30 +292,107 @@ __device__ __forceinline__ void faccum(FSite &s, double fi) {
     if constexpr (cz(I) < 0) s.jz = M::sub(s.jz, fi);
 }
 
+// Filtered potential force along one axis (oracle orc_potential_force):
+//   h(x) = -(phi(x) * ((mu(x+1) - mu(x-1)) * 0.5)),
+//   F = ((h(x-1) + h(x+1)) + (h(x) + h(x))) * 0.25,
+// from phi at x, x+-1 and mu at x, x+-1, x+-2 along the axis.
+__device__ __forceinline__ double force_axis(double ph0, double php, double phm, double mu0,
+                                             double mp1, double mm1, double mp2, double mm2) {
+    using M = Exact;
+    const double h0 = -M::mul(ph0, M::mul(M::sub(mp1, mm1), 0.5));
+    const double hp = -M::mul(php, M::mul(M::sub(mp2, mu0), 0.5));
+    const double hm = -M::mul(phm, M::mul(M::sub(mu0, mm2), 0.5));
+    return M::mul(M::add(M::add(hm, hp), M::add(h0, h0)), 0.25);
+}
+
+// physics 1: mu(x) and the filtered potential force at lane k of the chunk,
+// from the phi and mu slabs.  phi(x) from the slab equals the in-register sum
+// of the pulled g bitwise (k_phi forms it from the same state in index order).
+template <int VVL>
+struct ForcePot {
+    const FluidArgs &a;
+    const Pos &p;
+    __device__ __forceinline__ void operator()(int k, double &mu, double &Fx, double &Fy,
+                                               double &Fz) const {
+        const int x = p.x0 + k, nx = a.nx, ny = a.ny;
+        const long long PL = a.PL;
+        const double *pc = a.phi + (long long)(p.z + 1) * PL + (long long)p.y * nx;
+        const double *mc = a.mu + (long long)(p.z + 2) * PL + (long long)p.y * nx;
+        const int xp1 = wrapi(x + 1, nx), xm1 = wrapi(x - 1, nx);
+        const int xp2 = wrap2(x + 2, nx), xm2 = wrap2(x - 2, nx);
+        const long long yp1 = (long long)(wrapi(p.y + 1, ny) - p.y) * nx,
+                        ym1 = (long long)(wrapi(p.y - 1, ny) - p.y) * nx,
+                        yp2 = (long long)(wrap2(p.y + 2, ny) - p.y) * nx,
+                        ym2 = (long long)(wrap2(p.y - 2, ny) - p.y) * nx;
+        const double ph0 = __ldg(pc + x);
+        mu = __ldg(mc + x);
+        Fx = force_axis(ph0, __ldg(pc + xp1), __ldg(pc + xm1), mu, __ldg(mc + xp1),
+                        __ldg(mc + xm1), __ldg(mc + xp2), __ldg(mc + xm2));
+        Fy = force_axis(ph0, __ldg(pc + yp1 + x), __ldg(pc + ym1 + x), mu, __ldg(mc + yp1 + x),
+                        __ldg(mc + ym1 + x), __ldg(mc + yp2 + x), __ldg(mc + ym2 + x));
+        Fz = force_axis(ph0, __ldg(pc + PL + x), __ldg(pc - PL + x), mu, __ldg(mc + PL + x),
+                        __ldg(mc - PL + x), __ldg(mc + 2 * PL + x), __ldg(mc - 2 * PL + x));
+    }
+};
+
+// physics 2: mu(x) and the stress-divergence force at lane k (oracle
+// stress_force op order): F_a = -((D_x P_ax + D_y P_ay) + D_z P_az),
+// D_b h = (h(+b) - h(-b)) * 0.5, P_aa = p_iso + ((kappa g_a) g_a),
+// P_ab = (kappa g_a) g_b, from the aux arrays the mu kernel wrote.
+template <int VVL>
+struct ForceStress {
+    const FluidArgs &a;
+    const Pos &p;
+    __device__ __forceinline__ void operator()(int k, double &mu, double &Fx, double &Fy,
+                                               double &Fz) const {
+        using M = Exact;
+        const long long PL = a.PL, as = a.astride;
+        const int x = p.x0 + k;
+        const long long r = (long long)(p.z + 2) * PL + (long long)p.y * a.nx;
+        const long long c = r + x;
+        const long long sp[3] = {r + wrapi(x + 1, a.nx),
+                                 (long long)(p.z + 2) * PL + (long long)wrapi(p.y + 1, a.ny) * a.nx + x,
+                                 c + PL};
+        const long long sm[3] = {r + wrapi(x - 1, a.nx),
+                                 (long long)(p.z + 2) * PL + (long long)wrapi(p.y - 1, a.ny) * a.nx + x,
+                                 c - PL};
+        mu = __ldg(a.mu + c);
+        const double *piso = a.aux, *g[3] = {a.aux + as, a.aux + 2 * as, a.aux + 3 * as};
+        double F[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double dd[3];
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+                double tp = M::mul(M::mul(a.kappa, __ldg(g[d] + sp[b])), __ldg(g[b] + sp[b]));
+                double tm = M::mul(M::mul(a.kappa, __ldg(g[d] + sm[b])), __ldg(g[b] + sm[b]));
+                if (d == b) {
+                    tp = M::add(__ldg(piso + sp[b]), tp);
+                    tm = M::add(__ldg(piso + sm[b]), tm);
+                }
+                dd[b] = M::mul(M::sub(tp, tm), 0.5);
+            }
+            F[d] = -M::add(M::add(dd[0], dd[1]), dd[2]);
+        }
+        Fx = F[0];
+        Fy = F[1];
+        Fz = F[2];
+    }
+};
+
 // Site-wide quantities after the moments (oracle collide_site op order).
 template <int MODE, int PHYS>
-__device__ __forceinline__ void fsite_finish(FSite &s, double gmx, double gmy, double gmz,
-                                             const FluidArgs &a) {
+__device__ __forceinline__ void fsite_finish(FSite &s, const FluidArgs &a) {
     using M = Exact;
     if constexpr (MODE == LTK_MODE_EXACT) {
+        const double rr = __drcp_rn(s.rho);  // RN(1/rho): three divisions by rho
         if constexpr (PHYS >= 1) {
-            if constexpr (PHYS == 1) {
-                s.Fx = -M::mul(s.phi, gmx);
-                s.Fy = -M::mul(s.phi, gmy);
-                s.Fz = -M::mul(s.phi, gmz);
-            } else {  // the stress-divergence force itself
-                s.Fx = gmx;
-                s.Fy = gmy;
-                s.Fz = gmz;
-            }
-            const double rr = __drcp_rn(s.rho);  // RN(1/rho): three divisions by rho
             s.ux = div_rcp(M::add(s.jx, M::mul(0.5, s.Fx)), s.rho, rr);
             s.uy = div_rcp(M::add(s.jy, M::mul(0.5, s.Fy)), s.rho, rr);
             s.uz = div_rcp(M::add(s.jz, M::mul(0.5, s.Fz)), s.rho, rr);
             s.uF = M::add(M::add(M::mul(s.ux, s.Fx), M::mul(s.uy, s.Fy)), M::mul(s.uz, s.Fz));
             s.psi = M::sub(M::mul(a.gamma, s.mu), M::mul(s.phi, a.cs2));
         } else {
-            const double rr = __drcp_rn(s.rho);
             s.ux = div_rcp(s.jx, s.rho, rr);
             s.uy = div_rcp(s.jy, s.rho, rr);
             s.uz = div_rcp(s.jz, s.rho, rr);
@@ -282,15 +403,6 @@ __device__ __forceinline__ void fsite_finish(FSite &s, double gmx, double gmy, d
     } else {
         const double inv = 1.0 / s.rho;
         if constexpr (PHYS >= 1) {
-            if constexpr (PHYS == 1) {
-                s.Fx = -(s.phi * gmx);
-                s.Fy = -(s.phi * gmy);
-                s.Fz = -(s.phi * gmz);
-            } else {
-                s.Fx = gmx;
-                s.Fy = gmy;
-                s.Fz = gmz;
-            }
             s.ux = fma(0.5, s.Fx, s.jx) * inv;
             s.uy = fma(0.5, s.Fy, s.jy) * inv;
             s.uz = fma(0.5, s.Fz, s.jz) * inv;
@@ -373,95 +485,15 @@ __device__ __forceinline__ void frelax_pair(double (&F)[Q][VVL], double (&G)[Q][
     if constexpr (O != C) frelax<O, MODE, PHYS, T1>(F[O][k], G[O][k], -q, sq, s2, s, a);
 }
 
-// One VVL-site chunk of the pull + forced collision.  HINT bit 0: the input
-// state is read with L2 evict-first (each value is pulled once); bit 1: f' is
-// stored evict-first and g' evict-last, so g' stays in L2 until k_cs_phi's
-// lagged phi re-reads it a few planes later.
-template <int VVL, int HINT>
-__device__ __forceinline__ void cs_load(const FluidArgs &a, const Pos &p, double (&F)[Q][VVL],
-                                        double (&G)[Q][VVL]) {
-    const uint64_t pol = (HINT & 1) ? l2_evict_first() : 0;
-    constexpr int LD = (HINT & 1) ? kLdNc : kLdg;
-    static_for<0, Q>([&](auto I) { pull<I.value, VVL, LD>(F[I.value], a.f_in, a, p, pol); });
-    static_for<0, Q>([&](auto I) { pull<I.value, VVL, LD>(G[I.value], a.g_in, a, p, pol); });
-}
-
-// mu and its central gradient at lane k of the chunk, from the mu slab in
-// global memory: mu(x), ((mu(x+1) - mu(x-1)) * 0.5) per axis (oracle op order).
-template <int VVL>
-struct MuGlobal {
-    const FluidArgs &a;
-    const Pos &p;
-    __device__ __forceinline__ void operator()(int k, double &mu, double &gmx, double &gmy,
-                                               double &gmz) const {
-        const double *mc = a.mu + (long long)(p.z + 1) * a.PL;
-        const int yp = wrapi(p.y + 1, a.ny), ym = wrapi(p.y - 1, a.ny);
-        const int x = p.x0 + k;
-        const long long r = (long long)p.y * a.nx;
-        mu = __ldg(mc + r + x);
-        gmx = Exact::mul(Exact::sub(__ldg(mc + r + wrapi(x + 1, a.nx)),
-                                    __ldg(mc + r + wrapi(x - 1, a.nx))), 0.5);
-        gmy = Exact::mul(Exact::sub(__ldg(mc + (long long)yp * a.nx + x),
-                                    __ldg(mc + (long long)ym * a.nx + x)), 0.5);
-        gmz = Exact::mul(Exact::sub(__ldg(mc + a.PL + r + x), __ldg(mc - a.PL + r + x)), 0.5);
-    }
-};
-
-// physics 2: mu(x) and the stress-divergence force at lane k (oracle
-// stress_force op order): F_a = -((D_x P_ax + D_y P_ay) + D_z P_az),
-// D_b h = (h(+b) - h(-b)) * 0.5, P_aa = p_iso + ((kappa g_a) g_a),
-// P_ab = (kappa g_a) g_b, from the aux arrays the mu kernel wrote.
-template <int VVL>
-struct StressGlobal {
-    const FluidArgs &a;
-    const Pos &p;
-    __device__ __forceinline__ void operator()(int k, double &mu, double &Fx, double &Fy,
-                                               double &Fz) const {
-        using M = Exact;
-        const long long PL = a.PL, as = a.astride;
-        const long long c = (long long)(p.z + 1) * PL + (long long)p.y * a.nx + (p.x0 + k);
-        const int x = p.x0 + k;
-        // neighbour offsets from the centre: +-x (periodic), +-y (periodic), +-z (halo planes)
-        const long long r = (long long)(p.z + 1) * PL + (long long)p.y * a.nx;
-        const long long sp[3] = {r + wrapi(x + 1, a.nx),
-                                 (long long)(p.z + 1) * PL + (long long)wrapi(p.y + 1, a.ny) * a.nx + x,
-                                 c + PL};
-        const long long sm[3] = {r + wrapi(x - 1, a.nx),
-                                 (long long)(p.z + 1) * PL + (long long)wrapi(p.y - 1, a.ny) * a.nx + x,
-                                 c - PL};
-        mu = __ldg(a.mu + c);
-        const double *piso = a.aux, *g[3] = {a.aux + as, a.aux + 2 * as, a.aux + 3 * as};
-        double F[3];
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            double dd[3];
-#pragma unroll
-            for (int b = 0; b < 3; ++b) {
-                double tp = M::mul(M::mul(a.kappa, __ldg(g[d] + sp[b])), __ldg(g[b] + sp[b]));
-                double tm = M::mul(M::mul(a.kappa, __ldg(g[d] + sm[b])), __ldg(g[b] + sm[b]));
-                if (d == b) {
-                    tp = M::add(__ldg(piso + sp[b]), tp);
-                    tm = M::add(__ldg(piso + sm[b]), tm);
-                }
-                dd[b] = M::mul(M::sub(tp, tm), 0.5);
-            }
-            F[d] = -M::add(M::add(dd[0], dd[1]), dd[2]);
-        }
-        Fx = F[0];
-        Fy = F[1];
-        Fz = F[2];
-    }
-};
-
-template <int VVL, int MODE, int PHYS, int T1, int HINT, class MuFn>
-__device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, double (&F)[Q][VVL],
-                                          double (&G)[Q][VVL], const MuFn &mufn) {
+// One VVL-site chunk: pull f, g (38 values per site held in registers, one
+// HBM read + one write each), force and mu from the stencils, collide, store
+// aligned, plus the halo images of the components that cross a z face.
+template <int VVL, int MODE, int PHYS, int T1>
+__device__ __forceinline__ void cs_site(const FluidArgs &a, const Pos &p) {
     using M = typename std::conditional<MODE == LTK_MODE_EXACT, Exact, Fast>::type;
-    uint64_t pol_first = 0, pol_last = 0;
-    if constexpr (HINT & 2) {
-        pol_first = l2_evict_first();
-        pol_last = l2_evict_last();
-    }
+    double F[Q][VVL], G[Q][VVL];
+    static_for<0, Q>([&](auto I) { pull<I.value, VVL>(F[I.value], a.f_in, a, p); });
+    static_for<0, Q>([&](auto I) { pull<I.value, VVL>(G[I.value], a.g_in, a, p); });
 
     FSite st[VVL];
 #pragma unroll
@@ -476,11 +508,11 @@ __device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, doub
     for (int k = 0; k < VVL; ++k) {
 #pragma unroll
         for (int i = 0; i < Q; ++i) st[k].phi = M::add(st[k].phi, G[i][k]);
-        double gmx = 0.0, gmy = 0.0, gmz = 0.0;
-        if constexpr (PHYS >= 1) mufn(k, st[k].mu, gmx, gmy, gmz);
+        if constexpr (PHYS == 1) ForcePot<VVL>{a, p}(k, st[k].mu, st[k].Fx, st[k].Fy, st[k].Fz);
+        if constexpr (PHYS == 2) ForceStress<VVL>{a, p}(k, st[k].mu, st[k].Fx, st[k].Fy, st[k].Fz);
         ok[k] = !(st[k].rho <= 0.0);
         if (ok[k]) {
-            fsite_finish<MODE, PHYS>(st[k], gmx, gmy, gmz, a);
+            fsite_finish<MODE, PHYS>(st[k], a);
         } else {  // leave the streamed values; report the site in host order
             const long long zg = a.z0 + p.z;
             const long long site = ((long long)(p.x0 + k) * a.ny + p.y) * a.nz_global + zg;
@@ -494,16 +526,11 @@ __device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, doub
             if (ok[k]) frelax_pair<C, MODE, PHYS, T1, VVL>(F, G, k, st[k], a);
     });
 
-    const long long off = (long long)p.y * a.SY + p.x0;       // row offset inside a plane
+    const long long off = (long long)p.y * a.SY + p.x0;  // row offset inside a plane
     const long long o = (long long)(p.z + 1) * a.SZ + off;
     static_for<0, Q>([&](auto I) {
-        if constexpr (HINT & 2) {
-            store_vec_pol<VVL>(a.f_out + I.value * a.SI + o, F[I.value], pol_first);
-            store_vec_pol<VVL>(a.g_out + I.value * a.SI + o, G[I.value], pol_last);
-        } else {
-            store_vec<VVL>(a.f_out + I.value * a.SI + o, F[I.value]);
-            store_vec<VVL>(a.g_out + I.value * a.SI + o, G[I.value]);
-        }
+        store_vec<VVL>(a.f_out + I.value * a.SI + o, F[I.value]);
+        store_vec<VVL>(a.g_out + I.value * a.SI + o, G[I.value]);
         // halo images of the components that cross the z faces
         if constexpr (cz(I.value) < 0) {
             if (p.z == 0 && a.img_f_dn) {
@@ -523,103 +550,11 @@ __device__ __forceinline__ void cs_finish(const FluidArgs &a, const Pos &p, doub
         __threadfence_system();  // peer images visible before the progress signal
 }
 
-template <int VVL, int MODE, int PHYS, int T1, int HINT>
-__device__ __forceinline__ void cs_site(const FluidArgs &a, const Pos &p) {
-    double F[Q][VVL], G[Q][VVL];
-    cs_load<VVL, HINT>(a, p, F, G);
-    if constexpr (PHYS == 2) cs_finish<VVL, MODE, PHYS, T1, HINT>(a, p, F, G, StressGlobal<VVL>{a, p});
-    else cs_finish<VVL, MODE, PHYS, T1, HINT>(a, p, F, G, MuGlobal<VVL>{a, p});
-}
-
-template <int VVL, int MODE, int PHYS, int T1, int HINT = 0>
+template <int VVL, int MODE, int PHYS, int T1>
 __global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_collide_stream(const FluidArgs a) {
     Pos p;
     if (!thread_pos<VVL>(a, p)) return;
-    cs_site<VVL, MODE, PHYS, T1, HINT>(a, p);
-}
-
-// ------------------------------------------------------------------ fused step
-// k_cs_phi: collide-stream of planes [z_lo, z_lo + nplanes) AND phi of the
-// NEXT state on planes [phi_lo, phi_hi), read back a few planes behind the
-// collision front -- the k_phi pass over g' leaves the step.
-// phi(x) = sum_i g'_i(x - c_i) reads g' on planes z-1..z+1, all written by
-// this launch, so:
-//  * work order: each CTA takes a ticket T (one atomicAdd); b = T mod ncta is
-//    its work index, so every lower index of this launch is already resident
-//    or finished; e = T div ncta counts this engine's launches (graph-replay
-//    safe: counters are never reset, every launch takes exactly ncta tickets);
-//  * warp w of CTA b handles collide threads [128 b + 32 w, +32) and the phi
-//    threads lag_ctas*128 behind.  A warp first issues its collision loads,
-//    then polls (ld.acquire) the completion counters of the planes its phi
-//    sites pull from, then issues the phi loads (L2), then finishes the
-//    collision and publishes its sites per plane (__syncwarp + one
-//    red.release per plane).  No CTA barrier after the ticket: warps never
-//    idle waiting for each other, so HBM requests stay in flight.
-//  * lag_ctas covers > 3 planes + one CTA (host-checked), so the waited-on
-//    planes belong to lower work indices: no deadlock; the host adds slack
-//    planes so the poll is normally satisfied at once.
-// Counters are 64-bit and cumulative: plane z is complete in launch e when
-// done[z] >= (e + 1) * tpp.  phi arithmetic is phi_site's (index-order
-// __dadd_rn): bitwise equal to k_phi.  phi planes never include 0 or nzl-1
-// (no halo images from here; the engine forms those planes with k_phi).
-__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void red_release_gpu_add(unsigned long long *p, unsigned long long v) {
-    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-template <int VVL, int MODE, int PHYS, int T1, int HINT>
-__global__ void __launch_bounds__(128, VVL == 1 ? 4 : 1) k_cs_phi(const FluidArgs a) {
-    __shared__ unsigned long long s_ticket;
-    unsigned long long *const ticket = a.sync, *const done = a.sync + 1;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(ticket, 1ull);
-    __syncthreads();
-    const unsigned long long T = s_ticket;
-    const unsigned b = (unsigned)(T % a.ncta);
-    const unsigned long long target = (T / a.ncta + 1) * (unsigned long long)a.tpp;
-    const long long tpp = a.tpp;
-    const int lane = threadIdx.x & 31;
-    const long long tw = (long long)b * 128 + (threadIdx.x & ~31);  // warp's first thread
-
-    // ---- collision loads of this warp's sites
-    const long long t = tw + lane;
-    const bool has_cs = b < a.ncta_cs && t < a.nthreads;
-    Pos pc;
-    double F[Q][VVL], G[Q][VVL];
-    if (has_cs) {
-        pos_of<VVL>(a, (unsigned)t, a.z_lo, pc);
-        cs_load<VVL, HINT>(a, pc, F, G);
-    }
-    // ---- phi of the next state, lag_ctas CTAs behind
-    const long long nphi = (long long)(a.phi_hi - a.phi_lo) * tpp;
-    const long long uw = tw - (long long)a.lag_ctas * 128;
-    if (uw >= 0 && uw < nphi) {  // warp-uniform
-        const long long u = uw + lane;
-        const long long ul = (uw + 32 < nphi ? uw + 32 : nphi) - 1;
-        const int zlo = a.phi_lo + (int)(uw / tpp) - 1, zhi = a.phi_lo + (int)(ul / tpp) + 1;
-        if (lane <= zhi - zlo) {
-            while (ld_acquire_gpu_u64(done + zlo + lane) < target) __nanosleep(64);
-        }
-        __syncwarp();
-        if (u < nphi) {
-            Pos p;
-            pos_of<VVL>(a, (unsigned)u, a.phi_lo, p);
-            phi_site<VVL, kLdCg, false>(a, p, a.g_out, a.phi_next, l2_evict_first());
-        }
-    }
-    if (has_cs) cs_finish<VVL, MODE, PHYS, T1, HINT>(a, pc, F, G, MuGlobal<VVL>{a, pc});
-    // ---- publish this warp's sites, one release per plane
-    __syncwarp();
-    if (b < a.ncta_cs && tw < a.nthreads) {
-        const int z = has_cs ? (int)(t / tpp) : -1;
-        const unsigned act = __ballot_sync(0xffffffffu, has_cs);
-        const unsigned same = __match_any_sync(0xffffffffu, z);
-        if (has_cs && lane == __ffs(same & act) - 1)
-            red_release_gpu_add(done + a.z_lo + z, (unsigned long long)__popc(same & act));
-    }
+    cs_site<VVL, MODE, PHYS, T1>(a, p);
 }
 
 }  // namespace ltk

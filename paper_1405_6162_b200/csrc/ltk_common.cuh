@@ -30,17 +30,28 @@ void count_launch(int n = 1);
         ltk::count_launch();                                    \
     } while (0)
 
+#define LTK_RC0(x)            \
+    do {                      \
+        int rc_ = (x);        \
+        if (rc_) return rc_;  \
+    } while (0)
+
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Device error word: lowest real site with rho <= 0 (INT64_MAX = none).
-// Defined in runtime.cu; declared extern for the kernels (relocatable code
-// is not used, so kernels call ltk::flag_singular via a pointer obtained at
-// launch time).
-long long *singular_word();
+// Device error words: 0 = no error, else LLONG_MAX - (lowest real site with
+// rho <= 0), so the lowest site wins an atomicMax and a reset is a memset.
+// Each CUDA stream has its own word (stream_word, runtime.cu) and each fluid
+// engine owns one, so errors are reported to the caller whose kernels met
+// them, never to another engine or device object sharing the GPU.
+long long *stream_word(cudaStream_t st);
+void release_stream_word(cudaStream_t st);
+// Read the word on `st` (after the work that may set it), reset it, and
+// return the site it records or -1.  Stream-ordered copies only.
+int take_word(long long *word, cudaStream_t st, long long *site);
 
 __device__ __forceinline__ void flag_singular(long long *word, long long site) {
-    atomicMin(reinterpret_cast<unsigned long long *>(word),
-              static_cast<unsigned long long>(site));
+    atomicMax(reinterpret_cast<unsigned long long *>(word),
+              static_cast<unsigned long long>(0x7fffffffffffffffLL - site));
 }
 
 // ---------------------------------------------------------------- D3Q19
@@ -166,101 +177,6 @@ __device__ __forceinline__ void store_vec(double *p, const double (&src)[VVL]) {
 #pragma unroll
         for (int k = 0; k < VVL; k += 2)
             *reinterpret_cast<double2 *>(p + k) = make_double2(src[k], src[k + 1]);
-    }
-}
-
-// ---------------------------------------------------------------- L2 cache policies
-// createpolicy handles for per-access L2 eviction priority (sm_80+ PTX).
-__device__ __forceinline__ uint64_t l2_evict_first() {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ uint64_t l2_evict_last() {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-
-// Read-only (nc) load with an L2 policy: the kernel's input state.
-__device__ __forceinline__ double ld_nc_pol(const double *p, uint64_t pol) {
-    double v;
-    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ double2 ld_nc_pol2(const double *p, uint64_t pol) {
-    double2 v;
-    asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-        : "=d"(v.x), "=d"(v.y)
-        : "l"(p), "l"(pol));
-    return v;
-}
-
-// L2-only (cg) load of data written earlier in the same launch by another CTA
-// (never through the non-coherent L1).  volatile + memory clobber: never
-// hoisted above the barrier that follows the producer's completion check.
-__device__ __forceinline__ double ld_cg_pol(const double *p, uint64_t pol) {
-    double v;
-    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;"
-                 : "=d"(v)
-                 : "l"(p), "l"(pol)
-                 : "memory");
-    return v;
-}
-__device__ __forceinline__ double2 ld_cg_pol2(const double *p, uint64_t pol) {
-    double2 v;
-    asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                 : "=d"(v.x), "=d"(v.y)
-                 : "l"(p), "l"(pol)
-                 : "memory");
-    return v;
-}
-
-__device__ __forceinline__ void st_pol(double *p, double v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol)
-                 : "memory");
-}
-__device__ __forceinline__ void st_pol2(double *p, double x, double y, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(x), "d"(y),
-                 "l"(pol)
-                 : "memory");
-}
-
-template <int VVL>
-__device__ __forceinline__ void load_vec_nc(double (&dst)[VVL], const double *p, uint64_t pol) {
-    if constexpr (VVL == 1) {
-        dst[0] = ld_nc_pol(p, pol);
-    } else {
-#pragma unroll
-        for (int k = 0; k < VVL; k += 2) {
-            double2 t = ld_nc_pol2(p + k, pol);
-            dst[k] = t.x;
-            dst[k + 1] = t.y;
-        }
-    }
-}
-
-template <int VVL>
-__device__ __forceinline__ void load_vec_cg(double (&dst)[VVL], const double *p, uint64_t pol) {
-    if constexpr (VVL == 1) {
-        dst[0] = ld_cg_pol(p, pol);
-    } else {
-#pragma unroll
-        for (int k = 0; k < VVL; k += 2) {
-            double2 t = ld_cg_pol2(p + k, pol);
-            dst[k] = t.x;
-            dst[k + 1] = t.y;
-        }
-    }
-}
-
-template <int VVL>
-__device__ __forceinline__ void store_vec_pol(double *p, const double (&src)[VVL], uint64_t pol) {
-    if constexpr (VVL == 1) {
-        st_pol(p, src[0], pol);
-    } else {
-#pragma unroll
-        for (int k = 0; k < VVL; k += 2) st_pol2(p + k, src[k], src[k + 1], pol);
     }
 }
 

@@ -6,6 +6,8 @@
 // (pkg/src/latkit/execution.py:271-281).  The reference's "target" is a host
 // arena; here it is B200 HBM.
 #include <atomic>
+#include <map>
+#include <utility>
 #include <climits>
 #include <cstring>
 #include <mutex>
@@ -33,22 +35,49 @@ int cuda_fail(cudaError_t err, const char *what) {
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-// One error word per device, allocated lazily (device memory, 8 bytes).
+// One error word per (device, stream), allocated on first use.
 static std::mutex g_word_mu;
-static long long *g_words[64] = {nullptr};
+static std::map<std::pair<int, cudaStream_t>, long long *> g_words;
 
-long long *singular_word() {
+long long *stream_word(cudaStream_t st) {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     std::lock_guard<std::mutex> lk(g_word_mu);
-    if (!g_words[dev]) {
-        long long *w = nullptr;
-        if (cudaMalloc(&w, sizeof(long long)) != cudaSuccess) return nullptr;
-        long long init = LLONG_MAX;
-        cudaMemcpy(w, &init, sizeof init, cudaMemcpyHostToDevice);
-        g_words[dev] = w;
+    auto key = std::make_pair(dev, st);
+    auto it = g_words.find(key);
+    if (it != g_words.end()) return it->second;
+    long long *w = nullptr;
+    if (cudaMalloc(&w, sizeof(long long)) != cudaSuccess) return nullptr;
+    // zeroed in stream order, before any kernel of `st` can use it
+    if (cudaMemsetAsync(w, 0, sizeof(long long), st) != cudaSuccess) {
+        cudaFree(w);
+        return nullptr;
     }
-    return g_words[dev];
+    g_words[key] = w;
+    return w;
+}
+
+void release_stream_word(cudaStream_t st) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    std::lock_guard<std::mutex> lk(g_word_mu);
+    auto it = g_words.find(std::make_pair(dev, st));
+    if (it == g_words.end()) return;
+    cudaFree(it->second);
+    g_words.erase(it);
+}
+
+int take_word(long long *word, cudaStream_t st, long long *site) {
+    *site = -1;
+    long long v = 0;
+    LTK_CUDA(cudaMemcpyAsync(&v, word, sizeof v, cudaMemcpyDeviceToHost, st));
+    LTK_CUDA(cudaStreamSynchronize(st));
+    if (v != 0) {
+        LTK_CUDA(cudaMemsetAsync(word, 0, sizeof v, st));
+        LTK_CUDA(cudaStreamSynchronize(st));
+        *site = LLONG_MAX - v;
+    }
+    return LTK_OK;
 }
 
 }  // namespace ltk
@@ -168,6 +197,8 @@ int ltk_stream_create(void **stream) {
 }
 
 int ltk_stream_destroy(void *stream) {
+    LTK_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    release_stream_word(as_stream(stream));
     LTK_CUDA(cudaStreamDestroy(as_stream(stream)));
     return LTK_OK;
 }
@@ -226,14 +257,13 @@ int ltk_stream_wait_event(void *stream, void *event) {
 
 int ltk_sync(void *stream, int64_t *site) {
     *site = -1;
-    LTK_CUDA(cudaStreamSynchronize(as_stream(stream)));
-    long long *w = singular_word();
-    if (!w) return fail(LTK_ERR_DEVICE, "device error word unavailable");
-    long long v = LLONG_MAX;
-    LTK_CUDA(cudaMemcpy(&v, w, sizeof v, cudaMemcpyDeviceToHost));
-    if (v != LLONG_MAX) {
-        long long reset = LLONG_MAX;
-        LTK_CUDA(cudaMemcpy(w, &reset, sizeof reset, cudaMemcpyHostToDevice));
+    cudaStream_t st = as_stream(stream);
+    LTK_CUDA(cudaStreamSynchronize(st));
+    long long *w = stream_word(st);
+    if (!w) return fail(LTK_ERR_DEVICE, "stream error word unavailable");
+    long long v = -1;
+    LTK_RC0(take_word(w, st, &v));
+    if (v >= 0) {
         *site = v;
         return fail(LTK_ERR_SINGULAR, "rho <= 0 at lattice site %lld", v);
     }

@@ -4,8 +4,10 @@ The reference stops at the collision (reference pkg/README.md:34-35); this
 module adds the timestep of SURVEY.md Appendix C, specified in DESIGN.md §2:
 
     stream (pull) -> phi = sum g -> mu = A phi + B phi^3 - kappa lap(phi)
-    -> Guo-forced collision of f with F = -phi grad(mu), g relaxed to an
-       equilibrium carrying the chemical potential.
+    -> Guo-forced collision of f with the potential force -phi grad(mu)
+       (each component filtered [1/4 1/2 1/4] along its own axis, which keeps
+       flat interfaces at rest: DESIGN.md §2), g relaxed to an equilibrium
+       carrying the chemical potential.
 
 `BinaryFluid` owns one z-slab (the whole lattice on one GPU) in the C++
 engine of csrc/fluid.cu and runs whole timesteps without Python in the loop.
@@ -31,15 +33,13 @@ from .model import D3Q19Model, Q
 
 MODE_EXACT = nat.MODE_EXACT
 MODE_FAST = nat.MODE_FAST
-CS_REG = nat.CS_REG
-CS_TMA = nat.CS_TMA
-MU_AUTO, MU_TMA, MU_PLAIN, MU_COL, MU_BLK = (nat.MU_AUTO, nat.MU_TMA, nat.MU_PLAIN,
-                                            nat.MU_COL, nat.MU_BLK)
+MU_AUTO, MU_PLAIN = nat.MU_AUTO, nat.MU_PLAIN
 LAYOUT_SOA, LAYOUT_ROW = nat.LAYOUT_SOA, nat.LAYOUT_ROW
 #: passive: the reference collision after streaming; binary: free-energy binary
-#: fluid with the force F = -phi grad(mu); binary-stress: the same fluid with the
-#: momentum-conserving F = -div P of the chemical pressure tensor (stable flat
-#: interfaces at Ludwig-scale constants where the potential form is not)
+#: fluid with the filtered potential force -phi grad(mu) (flat interfaces relax
+#: to rest); binary-stress: the same fluid with the momentum-conserving
+#: F = -div P of the chemical pressure tensor (Ludwig's divergence form; its
+#: discrete force is not zero at equilibrium: spurious currents ~1e-4)
 PHYSICS = {"passive": 0, "binary": 1, "binary-stress": 2}
 
 
@@ -169,17 +169,10 @@ class BinaryFluid:
     def set_graph(self, enable: bool) -> None:
         nat.check(nat.lib.ltk_fluid_use_graph(self._h, 1 if enable else 0), "use_graph")
 
-    def set_fuse(self, enable: bool, extra_lag: int = 1) -> None:
-        """Fused collide-stream + next-state phi (k_cs_phi; off by default, it
-        measured slower).  Bitwise identical either way; off runs the
-        three-kernel step."""
-        nat.check(nat.lib.ltk_fluid_set_fuse(self._h, 1 if enable else 0, int(extra_lag)),
-                  "set_fuse")
-
     def set_layout(self, layout: int | None = None) -> int:
         """f/g storage layout of this slab: LAYOUT_ROW (row-blocked: the 19
         components of an x-row adjacent; default for even nx, measured faster)
-        or LAYOUT_SOA (component-major planes; attach_nccl selects it).
+        or LAYOUT_SOA (component-major planes).  Every transport takes either.
         Bitwise identical results; set before load() and before attaching a
         transport.  Returns the previous layout (None only queries)."""
         prev = ctypes.c_int32()
@@ -209,6 +202,11 @@ class BinaryFluid:
         v = ctypes.c_int32(0)
         nat.check(nat.lib.ltk_fluid_peer_timeout(self._h, ctypes.byref(v)), "peer_timeout")
         return bool(v.value)
+
+    def inject_peer_timeout(self) -> None:
+        """Test hook: the next progress waits fail at once, as if a neighbour
+        had stalled; sync() then raises DeviceError."""
+        nat.check(nat.lib.ltk_fluid_inject_peer_timeout(self._h), "inject_peer_timeout")
 
     def attach_nccl(self, unique_id: bytes) -> None:
         if len(unique_id) != 128:
@@ -287,12 +285,12 @@ class BinaryFluid:
         ptrs = [ctypes.c_void_p() for _ in range(4)]
         nat.lib.ltk_fluid_buffers(self._h, *[ctypes.byref(p) for p in ptrs])
         out = []
-        for p in (ptrs[2], ptrs[3]):
-            a = np.empty((self.nzl + 2) * PL)
+        for p, halo in ((ptrs[2], 1), (ptrs[3], 2)):  # phi: 1 halo plane per face, mu: 2
+            a = np.empty((self.nzl + 2 * halo) * PL)
             nat.check(nat.lib.ltk_d2h(a.ctypes.data, p.value, a.nbytes, self.stream), "D2H")
-            out.append(a)
+            out.append(a[halo * PL:(self.nzl + halo) * PL].reshape(self.nzl, s.ny, s.nx))
         self.sync()
-        return tuple(a[PL:(self.nzl + 1) * PL].reshape(self.nzl, s.ny, s.nx) for a in out)
+        return tuple(out)
 
     def totals(self, allreduce=None) -> np.ndarray:
         """[sum rho, sum j_x, sum j_y, sum j_z, sum phi] of the current state on
@@ -311,10 +309,13 @@ class BinaryFluid:
         nat.check(nat.lib.ltk_fluid_run(self._h, int(nsteps), stream), "ltk_fluid_run")
         self.steps_done += int(nsteps)
 
-    def sync(self, stream: int | None = None) -> None:
-        """Wait for the engine stream; raise SingularStateError on rho <= 0."""
+    def sync(self) -> None:
+        """Wait for the engine's streams and check its own error words:
+        SingularStateError on rho <= 0 (lowest site, host order), DeviceError
+        when a peer progress wait timed out (a neighbour slab stalled; the
+        engine then refuses further steps)."""
         site = ctypes.c_int64(-1)
-        rc = nat.lib.ltk_sync(self.stream if stream is None else stream, ctypes.byref(site))
+        rc = nat.lib.ltk_fluid_sync(self._h, ctypes.byref(site))
         if rc == nat.LTK_ERR_SINGULAR:
             raise SingularStateError(f"rho <= 0 at lattice site {site.value}")
         nat.check(rc, "sync")
@@ -327,21 +328,10 @@ class BinaryFluid:
         return [float(v) for v in arr]
 
 
-def cs_variant(variant: int | None = None) -> int:
-    """Collide-stream kernel used by every engine of the process: CS_REG
-    (register-resident loads) or CS_TMA (TMA-staged rows, warp-specialised).
-    Returns the previous value; None only queries."""
-    prev = ctypes.c_int32(0)
-    nat.check(nat.lib.ltk_fluid_cs_variant(-1 if variant is None else int(variant),
-                                           ctypes.byref(prev)), "cs_variant")
-    return int(prev.value)
-
-
 def mu_variant(variant: int | None = None) -> int:
-    """Chemical-potential stencil kernel of the process: MU_AUTO (the 2.5-D
-    shared-memory tile kernel k_mu_lds where it applies, else TMA, else plain),
-    MU_COL / MU_BLK (the register kernels k_mu_col / k_mu_blk instead of
-    k_mu_lds), MU_TMA, MU_PLAIN.
+    """Chemical-potential stencil kernel of the process: MU_AUTO (the
+    shared-memory tile kernel k_mu_tile where the shape allows it, else the
+    plain one) or MU_PLAIN.  Bitwise identical.
     Returns the previous value; None only queries."""
     prev = ctypes.c_int32(0)
     nat.check(nat.lib.ltk_fluid_mu_variant(-1 if variant is None else int(variant),

@@ -1,9 +1,10 @@
 """z-slab decomposition: geometry, the halo-exchange schedule, and a
 one-device multi-slab stepper.
 
-The production multi-GPU path is the C++ engine (csrc/fluid.cu,
-`enqueue_step` / `exchange`): one slab per rank, NCCL send/recv of the halo
-planes overlapped with the interior planes.  This module states the same
+The production multi-GPU path is the C++ engine (csrc/fluid.cu): one slab
+per rank, halo planes stored by the producing kernels into the neighbours
+over NVLink (peer transport) or NCCL send/recv (`exchange`), overlapped with
+the interior planes.  This module states the same
 decomposition in Python so that it can be checked without several GPUs:
 
 * `slab_bounds`, `halo_schedule` -- the ownership and the ordered
@@ -62,9 +63,14 @@ class HaloOp:
 def halo_schedule(kind: str, rank: int, nranks: int, nzl: int) -> list[HaloOp]:
     """Ordered ops of one exchange group, exactly as the engine issues them.
 
-    kind "fg": crossing components of f then g; "phi" / "mu": one plane each way.
-    Sends: top owned plane (zs = nzl) up, bottom owned plane (zs = 1) down.
-    Receives: from down into zs = 0, from up into zs = nzl + 1.
+    kind "fg": crossing components of f then g (the engine packs them into
+    one contiguous face per direction, in this order); "phi": one plane each
+    way; "mu": two planes each way (mu layout, zs = z + 2).
+    fg / phi sends: top owned plane (zs = nzl) up, bottom owned plane (zs = 1)
+    down; receives: from down into zs = 0, from up into zs = nzl + 1.
+    mu sends: planes zs = nzl, nzl + 1 up and zs = 2, 3 down; receives from
+    down into zs = 0, 1 and from up into zs = nzl + 2, nzl + 3 (`plane` is the
+    first of the pair).
     """
     up, down = neighbours(rank, nranks)
     ops: list[HaloOp] = []
@@ -77,9 +83,12 @@ def halo_schedule(kind: str, rank: int, nranks: int, nzl: int) -> list[HaloOp]:
             ops += [HaloOp("recv", down, d, c, 0) for c in CZ_UP]
         for d in ("f", "g"):
             ops += [HaloOp("recv", up, d, c, nzl + 1) for c in CZ_DOWN]
-    else:
+    elif kind == "phi":
         ops = [HaloOp("send", up, kind, 0, nzl), HaloOp("send", down, kind, 0, 1),
                HaloOp("recv", down, kind, 0, 0), HaloOp("recv", up, kind, 0, nzl + 1)]
+    else:
+        ops = [HaloOp("send", up, kind, 0, nzl), HaloOp("send", down, kind, 0, 2),
+               HaloOp("recv", down, kind, 0, 0), HaloOp("recv", up, kind, 0, nzl + 2)]
     return ops
 
 
@@ -119,6 +128,8 @@ class VirtualSlabs:
         nat.check(nat.lib.ltk_set_device(device))
         self.stream = nat.stream_create()
         z0, nzl = slab_bounds(shape.nz, 0, nslabs)
+        if nzl < 2:
+            raise ShapeError("z-slabs need >= 2 planes each (mu halos are 2 deep)")
         PL = shape.nx * shape.ny
         self.nzl, self.PL = nzl, PL
         cstride = -(-((nzl + 2) * PL) // 64) * 64
@@ -128,9 +139,10 @@ class VirtualSlabs:
         for _ in range(nslabs):
             b = {k: self._alloc(8 * Q * cstride) for k in ("fA", "gA", "fB", "gB")}
             b["phi"] = self._alloc(8 * (nzl + 2) * PL)
-            b["mu"] = self._alloc(8 * (nzl + 2) * PL)
+            b["mu"] = self._alloc(8 * (nzl + 4) * PL)
             self.bufs.append(b)
         self.face = self._alloc(8 * 10 * PL)
+        self._stage, self._stage_bytes = 0, 0
         self.cur = "A"
 
     def _alloc(self, nbytes: int) -> int:
@@ -146,7 +158,14 @@ class VirtualSlabs:
         nat.lib.ltk_stream_destroy(self.stream)
 
     def _staging(self, desc: FieldDescriptor) -> int:
-        return self._alloc(2 * desc.nbytes)
+        """One device staging buffer, reused by every load()/fields()."""
+        if 2 * desc.nbytes > self._stage_bytes:
+            if self._stage:
+                nat.check(nat.lib.ltk_stream_sync(self.stream))
+                self._ptrs.remove(self._stage)
+                nat.free(self._stage)
+            self._stage, self._stage_bytes = self._alloc(2 * desc.nbytes), 2 * desc.nbytes
+        return self._stage
 
     def load(self, f: Field, g: Field) -> None:
         desc = f.descriptor
@@ -195,12 +214,14 @@ class VirtualSlabs:
                                                         direction, self.stream))
 
     def _exchange_plane(self, key: str) -> None:
+        """phi: one plane per face (zs = z + 1); mu: two (zs = z + 2)."""
+        h = 1 if key == "phi" else 2
         nb = 8 * self.PL
         for r, b in enumerate(self.bufs):
             up, down = neighbours(r, self.P)
-            top, bot = b[key] + self.nzl * nb, b[key] + nb
-            nat.check(nat.lib.ltk_d2d(self.bufs[up][key], top, nb, self.stream))
-            nat.check(nat.lib.ltk_d2d(self.bufs[down][key] + (self.nzl + 1) * nb, bot, nb,
+            top, bot = b[key] + self.nzl * nb, b[key] + h * nb  # planes nzl-h.., 0..
+            nat.check(nat.lib.ltk_d2d(self.bufs[up][key], top, h * nb, self.stream))
+            nat.check(nat.lib.ltk_d2d(self.bufs[down][key] + (self.nzl + h) * nb, bot, h * nb,
                                       self.stream))
 
     def run(self, nsteps: int) -> None:
@@ -220,8 +241,8 @@ class VirtualSlabs:
                 self._exchange_plane("mu")
             for b in self.bufs:
                 nat.check(nat.lib.ltk_fluid_collide_stream(
-                    sl, b["f" + s], b["g" + s], b["mu"], b["f" + o], b["g" + o], prm, 0,
-                    self.nzl, self.vvl, self.stream), "collide_stream")
+                    sl, b["f" + s], b["g" + s], b["phi"], b["mu"], b["f" + o], b["g" + o], prm,
+                    0, self.nzl, self.vvl, self.stream), "collide_stream")
             self.cur = o
         site = ctypes.c_int64(-1)
         rc = nat.lib.ltk_sync(self.stream, ctypes.byref(site))

@@ -37,7 +37,7 @@ def test_ctypes_binding_covers_header():
     from paper_1405_6162_b200 import _native as nat
 
     assert set(nat.SIGNATURES) == declared()
-    assert nat.lib.ltk_abi_version() == 1
+    assert nat.lib.ltk_abi_version() == nat.ABI_VERSION == 2
 
 
 def test_struct_layouts_match_header():
@@ -82,7 +82,7 @@ int main(void) {
     int64_t site = -1;
     int n = 0;
     (void)p; (void)q; (void)site;
-    if (ltk_abi_version() != 1) return 1;
+    if (ltk_abi_version() != LTK_ABI_VERSION) return 1;
     if (ltk_device_count(&n) != LTK_OK && n != 0) return 2;
     printf("abi %d devices %d\n", ltk_abi_version(), n);
     return 0;
@@ -95,4 +95,4 @@ int main(void) {
                    check=True, capture_output=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr
-    assert out.stdout.startswith("abi 1")
+    assert out.stdout.startswith("abi 2")

@@ -74,14 +74,11 @@ def test_reference_arm_nonzero_rank_is_silent():
 
 
 def test_algorithmic_bytes_per_force_form():
-    # phi 160 + mu pass + collide-stream per site; fused: phi on the
-    # two boundary planes only
+    # phi 160 + mu pass + collide-stream per site
     sys.path.insert(0, ROOT)
     import bench
 
-    assert bench.step_bytes_per_site(False, 256, "binary") == 792
-    assert bench.step_bytes_per_site(False, 256, "binary-stress") == 856
-    assert bench.step_bytes_per_site(False, 256, "passive") == 768
-    assert bench.cs_bytes_per_site(False, "binary") == 616
-    assert bench.cs_bytes_per_site(True, "binary") == 624
-    assert bench.step_bytes_per_site(True, 256, "binary") == 624 + 16 + 160 * 2 / 256
+    assert bench.step_bytes_per_site("binary") == 800
+    assert bench.step_bytes_per_site("binary-stress") == 856
+    assert bench.step_bytes_per_site("passive") == 768
+    assert bench.cs_bytes_per_site("binary") == 624

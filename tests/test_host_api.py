@@ -151,8 +151,10 @@ class TestSlabSchedule:
             pairs = match_schedules(nranks, 4, kind)
             assert len(pairs) == nranks * (20 if kind == "fg" else 2)
             for send, receiver, recv in pairs:
-                # the top owned plane lands in the receiver's bottom halo and vice versa
-                assert (send.plane, recv.plane) in ((4, 0), (1, 5))
+                # the top owned plane(s) land in the receiver's bottom halo(s) and vice
+                # versa; mu moves two planes per face (mu layout zs = z + 2)
+                ok = ((4, 0), (2, 6)) if kind == "mu" else ((4, 0), (1, 5))
+                assert (send.plane, recv.plane) in ok
 
     def test_slab_bounds(self):
         from paper_1405_6162_b200.slabs import slab_bounds

@@ -1,8 +1,10 @@
 """Multi-rank z-slab decomposition on CPU: world_size 2 (and 3) over gloo.
 
-Each rank owns nz/P planes plus two halo planes, exchanges exactly the halo
-ops of slabs.halo_schedule (the order the C++ engine issues its NCCL
-send/recv), and steps its slab with the numpy restatement of the timestep.
+Each rank owns nz/P planes plus halo planes (one per face for f, g, phi; two
+for mu, which the filtered potential force reads at z +- 2), exchanges
+exactly the halo ops of slabs.halo_schedule (the order the C++ engine issues
+its NCCL send/recv), and steps its slab with the numpy restatement of the
+timestep.
 The gathered lattice must equal the single-domain oracle bitwise: this pins
 the decomposition, the crossing-component sets and the send/recv matching
 that the GPU engine relies on, with no GPU and no cluster.
@@ -37,7 +39,10 @@ def _exchange(dist, torch, arrays, ops, rank):
         tag = count.get(key, 0)
         count[key] = tag + 1
         a = arrays[op.kind]
-        view = a[op.comp, op.plane] if a.ndim == 4 else a[op.plane]
+        if op.kind == "mu":          # two planes per face
+            view = a[op.plane:op.plane + 2]
+        else:
+            view = a[op.comp, op.plane] if a.ndim == 4 else a[op.plane]
         if op.op == "send":
             reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(view)), op.peer, tag=tag))
         else:
@@ -77,7 +82,7 @@ def _worker(rank, world, port, out_q):
 
     f, g = to_slab(f0), to_slab(g0)
     phi = np.zeros((nzl + 2, ny, nx))
-    mu = np.zeros((nzl + 2, ny, nx))
+    mu = np.zeros((nzl + 4, ny, nx))      # mu layout: zs = z + 2
     cv = orc.CV
     for _ in range(STEPS):
         _exchange(dist, torch, {"f": f, "g": g}, halo_schedule("fg", rank, world, nzl), rank)
@@ -92,14 +97,19 @@ def _worker(rank, world, port, out_q):
         _exchange(dist, torch, {"phi": phi}, halo_schedule("phi", rank, world, nzl), rank)
         nb = [np.roll(ph, -1, 2), np.roll(ph, 1, 2), np.roll(ph, -1, 1), np.roll(ph, 1, 1),
               phi[2:nzl + 2], phi[0:nzl]]
-        mu[1:nzl + 1] = orc.mu_numpy(ph, nb, prm)
+        mu[2:nzl + 2] = orc.mu_numpy(ph, nb, prm)
         _exchange(dist, torch, {"mu": mu}, halo_schedule("mu", rank, world, nzl), rank)
-        m = mu[1:nzl + 1]
-        grad = [(np.roll(m, -1, 2) - np.roll(m, 1, 2)) * 0.5,
-                (np.roll(m, -1, 1) - np.roll(m, 1, 1)) * 0.5,
-                (mu[2:nzl + 2] - mu[0:nzl]) * 0.5]
+        m = mu[2:nzl + 2]
+        # filtered potential force (orc_potential_force op order); in z, h on
+        # planes -1..nzl from the phi halos and the two mu halo planes per face
+        force = []
+        for ax in (2, 1):   # x, y (in-plane, periodic)
+            h = -(ph * ((np.roll(m, -1, ax) - np.roll(m, 1, ax)) * 0.5))
+            force.append(((np.roll(h, 1, ax) + np.roll(h, -1, ax)) + (h + h)) * 0.25)
+        hz = -(phi[0:nzl + 2] * ((mu[2:nzl + 4] - mu[0:nzl + 2]) * 0.5))
+        force.append(((hz[0:nzl] + hz[2:nzl + 2]) + (hz[1:nzl + 1] + hz[1:nzl + 1])) * 0.25)
         fo, go = orc.collide_streamed_numpy(fs.reshape(19, -1), gs.reshape(19, -1), m.ravel(),
-                                            [gr.ravel() for gr in grad], prm)
+                                            [c.ravel() for c in force], prm)
         f = np.zeros_like(f)
         g = np.zeros_like(g)
         f[:, 1:nzl + 1] = fo.reshape(19, nzl, ny, nx)
