@@ -92,6 +92,8 @@ def parse_args(argv=None):
                    help="copy streams per PCIe direction in the e2e path")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-config1", action="store_true",
+                   help="skip the configs[1] collision-only 128^3 sub-record")
     p.add_argument("--seed", type=int, default=1234)
     p.add_argument("--layout", choices=("soa", "row"), default="row",
                    help="f/g storage: component-major planes (soa) or row-blocked (row: "
@@ -278,6 +280,29 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons), "source": "nvidia-smi -lms 20"}
 
 
+def device_pci(dev: int) -> str | None:
+    try:
+        import torch
+
+        p = torch.cuda.get_device_properties(dev)
+        return f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}"
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def p2p_matrix(devices: list[int]):
+    """{"devices": [...], "can_access": [[0/1]]}: cudaDeviceCanAccessPeer between
+    the devices the ranks run on (the peer transport needs every neighbour pair)."""
+    try:
+        import torch
+
+        m = [[1 if a == b else int(torch.cuda.can_device_access_peer(a, b)) for b in devices]
+             for a in devices]
+        return {"devices": devices, "can_access": m}
+    except Exception as exc:  # noqa: BLE001
+        return {"devices": devices, "error": str(exc)}
+
+
 def measured_hbm_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -320,6 +345,76 @@ def cpu_oracle_rate(shape, steps, seed, threads=None):
     return n * steps / dt / 1e6, threads, dt
 
 
+COLLISION_BYTES_PER_SITE = 608  # read + write f, g (reference bench.py:29)
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")
+
+
+def collision_config1(peak, peak_src, iters=50, vvls=(1, 2, 4, 8)):
+    """BASELINE configs[1] on the GPU: the reference collision kernel alone at
+    128^3 (EXACT, bitwise = reference), a VVL sweep through our latkit-API
+    benchmark_run (CUDA events around `iters` back-to-back launches; the
+    638 MB state is > L2, so no flush between launches)."""
+    import paper_1405_6162_b200 as lk
+    from paper_1405_6162_b200.bench import benchmark_run
+
+    shape = lk.LatticeShape(128, 128, 128)
+    sweep = []
+    for v in vvls:
+        r = benchmark_run("binary-collision", shape, v, iterations=iters, mode=lk.MODE_EXACT)
+        ms = r.elapsed_s / iters * 1e3
+        gbs = COLLISION_BYTES_PER_SITE * shape.nsites / (ms * 1e-3) / 1e9
+        sweep.append({"vvl": v, "ms_per_launch": ms, "mlups": r.sites_per_s / 1e6,
+                      "gb_s": gbs, "frac": gbs / peak})
+    best = max(sweep, key=lambda d: d["mlups"])
+    traffic = ncu_traffic("128x128x128", "exact", 1, "k_collide")
+    return {"workload": "BASELINE configs[1]: binary-collision kernel only, 128^3 fp64, "
+                        "EXACT (bitwise = reference), latkit benchmark_run on the device, "
+                        f"{iters} launches per VVL",
+            "vvl_sweep": sweep, "best_vvl": best["vvl"], "value": best["mlups"],
+            "unit": "MLUPS",
+            "roofline": {"bound": "hbm", "kernel": "k_collide", "achieved": best["gb_s"],
+                         "peak": peak, "unit": "GB/s", "frac": best["frac"],
+                         "traffic": traffic, "peak_source": peak_src,
+                         "bytes_per_site": COLLISION_BYTES_PER_SITE}}
+
+
+def reference_collision_cpu(budget_s=3.0, vvls=(1, 2, 4, 8), n=128):
+    """The reference's OWN CPU path for configs[1]: latkit.bench.benchmark_run
+    (reference pkg/src/latkit/bench.py:49-101) over the numba _collision_range
+    (kernels.py:89-125), backend "threaded" with every host core, imported from
+    the unmodified install in baseline/_ref.  One untimed run absorbs the numba
+    JIT; iterations per VVL are sized to ~budget_s."""
+    try:
+        if REF_PKG not in sys.path:
+            sys.path.insert(0, REF_PKG)
+        import latkit
+        from latkit.bench import benchmark_run as ref_run
+        from latkit.lattice import LatticeShape as RefShape
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"reference latkit not importable from baseline/_ref: {exc}"}
+    workers = os.cpu_count() or 1
+    try:
+        t0 = time.perf_counter()
+        ref_run("binary-collision", RefShape(16, 16, 16), 1, workers, "threaded", 1)
+        jit_s = time.perf_counter() - t0
+        shape = RefShape(n, n, n)
+        sweep = []
+        for v in vvls:
+            probe = ref_run("binary-collision", shape, v, workers, "threaded", 1)
+            iters = max(1, int(budget_s / max(probe.elapsed_s, 1e-6)))
+            r = ref_run("binary-collision", shape, v, workers, "threaded", iters)
+            sweep.append({"vvl": v, "iters": iters, "mlups": r.sites_per_s / 1e6,
+                          "gb_s": r.bandwidth_gb_s})
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"reference benchmark_run failed: {exc}"}
+    best = max(sweep, key=lambda d: d["mlups"])
+    return {"value": best["mlups"], "unit": "MLUPS", "cores": workers, "kind": "reference",
+            "sample": f"{n}^3 binary-collision, latkit {getattr(latkit, '__version__', '?')} "
+                      "benchmark_run (numba _collision_range), backend threaded, "
+                      f"best of VVL {list(vvls)}; numba JIT {jit_s:.1f} s untimed",
+            "best_vvl": best["vvl"], "vvl_sweep": sweep}
+
+
 # ----------------------------------------------------------------- reference arm
 
 def run_reference(args, rank, world):
@@ -357,6 +452,8 @@ def run_reference(args, rank, world):
                                    f"{steps} timesteps (oracle/lb_oracle.c orc_fluid_step)"},
         "e2e": {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        # BASELINE configs[1] on the reference's own code (numba), same box
+        "collision_128": None if args.no_config1 else reference_collision_cpu(),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -461,6 +558,14 @@ def run_ours(args, rank, world, local):
     ms_max = ctl.allreduce(ms, "MAX")
     launches_all = int(ctl.allreduce(float(launches), "SUM"))
 
+    # per-rank record (the driver checks N ranks really ran, on which devices)
+    me = {"rank": rank, "device": local, "pci_bus_id": device_pci(local), "ms": ms,
+          "ms_per_step": ms / args.steps, "transport": transport,
+          "peer_wait_timeout": bool(transport == "peer" and sim.peer_timed_out())}
+    ranks = [json.loads(b.rstrip(b"\0").decode())
+             for b in ctl.allgather_bytes(json.dumps(me).encode().ljust(512, b"\0"))]
+    p2p = p2p_matrix(sorted({r["device"] for r in ranks})) if rank == 0 and world > 1 else None
+
     total_sites = sites_rank * world
     value = total_sites * args.steps / (ms_max * 1e-3) / 1e6  # MLUPS
 
@@ -500,6 +605,11 @@ def run_ours(args, rank, world, local):
                          f"timesteps ({dt:.1f} s), oracle/lb_oracle.c orc_fluid_step"}
 
     sim.close()
+    coll = None
+    if rank == 0 and world == 1 and not args.no_config1:
+        coll = collision_config1(peak, peak_src)
+        if not args.no_cpu_baseline:
+            coll["cpu_baseline"] = reference_collision_cpu()
     if rank == 0:
         line = {
             "metric": "lattice site updates/sec (MLUPS), D3Q19 binary-fluid full timestep",
@@ -528,6 +638,8 @@ def run_ours(args, rank, world, local):
                        "halo_transport": ("periodic images (one slab)" if world == 1 else
                                           transport)},
             "gpu_launches": launches_all,
+            "ranks": ranks,
+            "p2p_access": p2p,
             "peer_wait_timeout": peer_timeout,
             "conservation": {"steps": args.warmup + args.steps,
                              "mass_rel_drift": abs(tot1[0] - tot0[0]) / abs(tot0[0]),
@@ -538,6 +650,7 @@ def run_ours(args, rank, world, local):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "collision_128": coll,
         }
         print(json.dumps(line), flush=True)
     ctl.close()
@@ -639,13 +752,33 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
                     "timed steps include the pipeline fill (first H2D) and drain (last D2H)"}
 
 
+def spawn_ranks(args, argv) -> int:
+    """`python bench.py --gpus N` without a launcher: re-run this script as N
+    ranks under torch.distributed.run (one process per GPU, rendezvous on
+    127.0.0.1), so the line is always an N-rank measurement, never a silent
+    one-rank run.  Rank 0's JSON line goes to this process's stdout."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+           "--nproc-per-node", str(args.gpus), "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)]
+    cmd += list(sys.argv[1:] if argv is None else argv)
+    return subprocess.call(cmd)
+
+
 def main(argv=None):
     args = parse_args(argv)
     if args.shape is None:
         args.shape = "512x512x512" if args.scaling == "strong" else "256x256x256"
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args, argv)
     rank, world, local = dist_env()
-    if args.gpus != world and world > 1:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {world}: launch "
+                         f"{args.gpus} ranks (torchrun) or pass --gpus {world}")
     if args.impl == "reference":
         return run_reference(args, rank, world)
     return run_ours(args, rank, world, local)

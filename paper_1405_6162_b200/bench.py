@@ -40,6 +40,9 @@ class BenchResult:
     sites_per_s: float
     bandwidth_gb_s: float
     counters: TransferCounters
+    #: threads per CUDA block actually launched (tpb rounded up to a warp, <= 256);
+    #: `tpb` above is the value requested, as the reference reports it
+    cuda_block: int = 0
 
 
 def benchmark_run(kernel_id: str, shape: LatticeShape, vvl: int, workers: int = 1,
@@ -80,8 +83,9 @@ def benchmark_run(kernel_id: str, shape: LatticeShape, vvl: int, workers: int = 
         target_free(b)
     sites_per_s = shape.nsites * iterations / elapsed
     result = BenchResult(kernel_id, backend, shape.nx, shape.ny, shape.nz, vvl, workers,
-                         plan.cuda_block, iterations, elapsed, sites_per_s,
-                         sites_per_s * BYTES_PER_SITE[kernel_id] / 1e9, device.counters)
+                         tpb, iterations, elapsed, sites_per_s,
+                         sites_per_s * BYTES_PER_SITE[kernel_id] / 1e9, device.counters,
+                         cuda_block=plan.cuda_block)
     device.close()
     return result
 

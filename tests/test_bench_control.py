@@ -67,10 +67,35 @@ def test_reference_arm_json_line():
 
 def test_reference_arm_nonzero_rank_is_silent():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2")
-    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--shape",
-                          "16x16x16", "--steps", "1", "--warmup", "1"], cwd=ROOT, env=env,
-                         capture_output=True, text=True, timeout=120)
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2",
+                          "--shape", "16x16x16", "--steps", "1", "--warmup", "1"], cwd=ROOT,
+                         env=env, capture_output=True, text=True, timeout=120)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_gpus_world_size_mismatch_is_an_error():
+    # --gpus N under a launcher with another WORLD_SIZE never runs silently
+    env = dict(os.environ, RANK="0", WORLD_SIZE="2")
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "4",
+                          "--shape", "16x16x16", "--steps", "1", "--warmup", "1",
+                          "--no-config1"], cwd=ROOT, env=env, capture_output=True, text=True,
+                         timeout=120)
+    assert out.returncode != 0 and "WORLD_SIZE 2" in out.stderr
+
+
+def test_gpus_without_launcher_spawns_ranks():
+    # `python bench.py --gpus 2` with no WORLD_SIZE re-runs itself as 2 ranks
+    # (torch.distributed.run on 127.0.0.1); rank 0 prints the one line
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2",
+                          "--shape", "16x16x16", "--steps", "1", "--warmup", "1",
+                          "--no-config1"], cwd=ROOT, env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2
 
 
 def test_algorithmic_bytes_per_force_form():

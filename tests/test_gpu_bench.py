@@ -40,7 +40,7 @@ def test_bench_line_contract():
         assert k in r, k
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and r["kernel"] == "k_collide_stream"
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
-    assert r["bytes_per_site"] == 616 and r["step_bytes_per_site"] == 792
+    assert r["bytes_per_site"] == 624 and r["step_bytes_per_site"] == 800
     c = d["cpu_baseline"]
     assert c["kind"] == "port" and c["value"] > 0 and c["cores"] >= 1 and c["sample"]
     e = d["e2e"]

@@ -141,6 +141,26 @@ class TestConstantsAndPlans:
                        for c in range(lo, hi)]
             assert covered == list(range(plan.chunk_count))
 
+    def test_reference_backend_schedules(self):
+        # the reference's own expectations (reference tests/test_execution.py:44-72)
+        P = lk.LaunchPlan
+        assert lk.backend_schedule(P(extent=64, vvl=8, workers=2), "threaded") == \
+            [[(0, 4)], [(4, 8)]]
+        assert lk.backend_schedule(P(extent=64, vvl=8, workers=1), "threaded") == [[(0, 8)]]
+        assert lk.backend_schedule(P(extent=56, vvl=8, workers=2), "threaded") == \
+            [[(0, 4)], [(4, 7)]]
+        assert lk.backend_schedule(P(extent=64, vvl=8), "reference") == [[(0, 8)]]
+        sched = lk.backend_schedule(P(extent=64, vvl=8, workers=2, tpb=4), "emulated")
+        assert sorted(r for w in sched for r in w) == [(0, 4), (4, 8)]
+        for backend in ("reference", "threaded", "emulated", "cuda"):
+            for workers in (1, 2, 3, 5):
+                plan = P(extent=112, vvl=8, workers=workers, tpb=3)
+                covered = sorted(c for w in lk.backend_schedule(plan, backend)
+                                 for lo, hi in w for c in range(lo, hi))
+                assert covered == list(range(plan.chunk_count))
+        with pytest.raises(lk.PlanError):
+            lk.backend_schedule(P(extent=64, vvl=8), "bogus")
+
 
 class TestSlabSchedule:
     @pytest.mark.parametrize("nranks", [1, 2, 3, 8])
