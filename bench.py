@@ -541,11 +541,18 @@ def run_ours(args, rank, world, local):
     ctl.barrier()
     sim.sync()
     l_before = nat.launch_count()
-    sim.profile(True)
+    ncu_range = os.environ.get("LTK_NCU_RANGE") == "1"  # ncu --replay-mode range
+    if ncu_range:
+        import torch
+
+        torch.cuda.profiler.start()
+    sim.profile(not ncu_range)
     nat.check(nat.lib.ltk_event_record(start, sim.stream))
     sim.run(args.steps)
     nat.check(nat.lib.ltk_event_record(stop, sim.stream))
     sim.sync()
+    if ncu_range:
+        torch.cuda.profiler.stop()
     prof = sim.profile(False)
     ms = nat.elapsed_ms(start, stop)
     tot1 = [ctl.allreduce(float(v), "SUM") for v in sim.totals()]
@@ -574,7 +581,7 @@ def run_ours(args, rank, world, local):
     peak, peak_src = measured_hbm_peak()
     kname = "k_collide_stream"
     cs_bytes = cs_bytes_per_site(args.physics)
-    achieved = cs_bytes * sites_rank / (cs_ms * 1e-3) / 1e9
+    achieved = cs_bytes * sites_rank / (max(cs_ms, 1e-9) * 1e-3) / 1e9
     # the committed ncu capture is of the binary form
     traffic = ncu_traffic(args.shape, args.mode, world, kname) if args.physics == "binary" else None
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved,

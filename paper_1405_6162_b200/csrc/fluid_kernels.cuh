@@ -133,6 +133,9 @@ __device__ __forceinline__ int modi(int v, int n) { return ((v % n) + n) % n; }
 
 template <class Store>
 __device__ __forceinline__ bool mu_images(const FluidArgs &a, int z, Store store) {
+    // only planes 0, 1, nzl-2, nzl-1 feed halo planes (any nzl): skip the
+    // source-plane arithmetic (two integer modulos per image) everywhere else
+    if (z >= 2 && z < a.nzl - 2) return false;
     bool img = false;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
