@@ -92,6 +92,9 @@ def parse_args(argv=None):
                    help="copy streams per PCIe direction in the e2e path")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--dump", default=None, metavar="PREFIX",
+                   help="after the timed steps, write the lattice state (reference field "
+                        "format, every rank its slab) to PREFIX.f / PREFIX.g (parity checks)")
     p.add_argument("--no-config1", action="store_true",
                    help="skip the configs[1] collision-only 128^3 sub-record")
     p.add_argument("--seed", type=int, default=1234)
@@ -226,6 +229,7 @@ class ClockSampler:
             except Exception:
                 self.smax = None
             self.done = threading.Event()
+            self.t0 = time.perf_counter()
             self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
             return
@@ -248,7 +252,8 @@ class ClockSampler:
             return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
                     "sm_max_mhz": self.smax,
                     "power_w_max": max(self.power) if self.power else None,
-                    "samples": len(self.sm), "reasons": reasons, "source": "nvml, 2 ms"}
+                    "samples": len(self.sm), "reasons": reasons, "source": "nvml, 2 ms",
+                    "window_ms": (time.perf_counter() - self.t0) * 1e3}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -536,10 +541,10 @@ def run_ours(args, rank, world, local):
 
     start, stop = nat.event_create(True), nat.event_create(True)
     clocks = ClockSampler(local)
-    if rank == 0:
-        clocks.start()
     ctl.barrier()
     sim.sync()
+    if rank == 0:
+        clocks.start()
     l_before = nat.launch_count()
     ncu_range = os.environ.get("LTK_NCU_RANGE") == "1"  # ncu --replay-mode range
     if ncu_range:
@@ -551,6 +556,7 @@ def run_ours(args, rank, world, local):
     sim.run(args.steps)
     nat.check(nat.lib.ltk_event_record(stop, sim.stream))
     sim.sync()
+    clk = clocks.stop() if rank == 0 else None  # samples from inside the timed region only
     if ncu_range:
         torch.cuda.profiler.stop()
     prof = sim.profile(False)
@@ -561,7 +567,6 @@ def run_ours(args, rank, world, local):
     peer_timeout = bool(transport == "peer" and sim.peer_timed_out())
     peer_timeout = ctl.allreduce(float(peer_timeout), "MAX") > 0
     ctl.barrier()
-    clk = clocks.stop() if rank == 0 else None
     ms_max = ctl.allreduce(ms, "MAX")
     launches_all = int(ctl.allreduce(float(launches), "SUM"))
 
@@ -596,10 +601,18 @@ def run_ours(args, rank, world, local):
                 "full_step_frac": step_bytes_per_site(args.physics) * sites_rank
                 / (ms / args.steps * 1e-3) / 1e9 / peak}
 
+    dumped = None
+    if args.dump:  # state after warmup + steps timesteps, before the e2e leg reloads it
+        from paper_1405_6162_b200.io import dump_state
+
+        dump_state(sim, args.dump, ctl.barrier)
+        dumped = {"prefix": args.dump, "steps": args.warmup + args.steps, "seed": args.seed}
+
     # ---------------- e2e: public API with host buffers, every step
-    e2e = None
+    e2e = e2e_job = None
     if not args.no_e2e and args.scaling == "weak":  # strong: 41 GB of state per 512^3 GPU
         e2e = run_e2e(args, sim, f0, g0, ctl, world, nat, lk)
+        e2e_job = run_e2e_job(args, sim, f0, g0, ctl, world, nat)
 
     # ---------------- CPU baseline (rank 0, N=1)
     cpu = None
@@ -657,7 +670,9 @@ def run_ours(args, rank, world, local):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_job": e2e_job,
             "collision_128": coll,
+            "dump": dumped,
         }
         print(json.dumps(line), flush=True)
     ctl.close()
@@ -774,6 +789,53 @@ def spawn_ranks(args, argv) -> int:
            "--master-port", str(port), os.path.abspath(__file__)]
     cmd += list(sys.argv[1:] if argv is None else argv)
     return subprocess.call(cmd)
+
+
+def run_e2e_job(args, sim, f0, g0, ctl, world, nat):
+    """A simulation job through the public API with host buffers: pinned
+    H2D of the initial state -> BinaryFluid.load_device -> run(K) -> store ->
+    D2H of the final state, all inside the timed region; K = --steps.  The
+    state crosses PCIe once each way per job (the reference's own benchmark
+    copies once at set-up and excludes it, pkg/src/latkit/bench.py:3-5)."""
+    from paper_1405_6162_b200.memory import pinned_empty, pinned_free
+
+    nelem = f0.data.size
+    nb = 8 * nelem
+    hin = [pinned_empty(nelem), pinned_empty(nelem)]
+    hin[0][:] = f0.data
+    hin[1][:] = g0.data
+    hout = [pinned_empty(nelem), pinned_empty(nelem)]
+    dev = nat.malloc(2 * nb)
+    cs, L, chk = sim.stream, nat.lib, nat.check
+    padded, nzl, K = f0.descriptor.padded_sites, sim.nzl, args.steps
+
+    def job():
+        for c in (0, 1):
+            chk(L.ltk_h2d(dev + c * nb, hin[c].ctypes.data, nb, cs))
+        sim.load_device(dev, dev + nb, padded, nzl, 0, cs)
+        sim.run(K)
+        sim.store_device(dev, dev + nb, padded, nzl, 0, cs)
+        for c in (0, 1):
+            chk(L.ltk_d2h(hout[c].ctypes.data, dev + c * nb, nb, cs))
+
+    job()  # warm-up (graph instantiation, first-touch of the pinned pages)
+    sim.sync()
+    ctl.barrier()
+    start, stop = nat.event_create(True), nat.event_create(True)
+    chk(L.ltk_event_record(start, cs))
+    job()
+    chk(L.ltk_event_record(stop, cs))
+    sim.sync()
+    ms = ctl.allreduce(nat.elapsed_ms(start, stop), "MAX")
+    nat.free(dev)
+    for arr in hin + hout:
+        pinned_free(arr)
+    sites = sim.shape.nx * sim.shape.ny * nzl * world
+    return {"value": sites * K / (ms * 1e-3) / 1e6, "unit": "MLUPS",
+            "h2d_bytes_per_step": 2 * nb / K, "d2h_bytes_per_step": 2 * nb / K,
+            "steps_per_job": K, "ms_per_job": ms,
+            "path": "pinned H2D(f,g) -> BinaryFluid.load_device -> run(K) -> store_device -> "
+                    "D2H(f,g), one job of K = --steps timesteps"}
 
 
 def main(argv=None):

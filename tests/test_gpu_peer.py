@@ -252,3 +252,61 @@ def test_stalled_neighbour_raises():
     finally:
         for sim in sims:
             sim.close()
+
+
+@pytest.mark.parametrize("transport", ["peer"])
+def test_bench_eight_ranks_bitwise(tmp_path, transport):
+    """`python bench.py --gpus 8` without a launcher: it
+    spawns 8 ranks itself, they share this test box's one GPU over the peer
+    transport, the line reports n_gpus 8 with one record per rank, and the
+    state dumped after the timed steps equals the oracle bitwise."""
+    import json
+    import subprocess
+    import sys
+
+    from oracle import oracle as orc
+    from paper_1405_6162_b200.kernels import random_binary_state
+    import paper_1405_6162_b200 as lk
+
+    nx, ny, nzl, world, seed = 16, 16, 4, 8, 77
+    prefix = str(tmp_path / "state")
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    out = subprocess.run([sys.executable, "bench.py", "--gpus", str(world), "--shape",
+                          f"{nx}x{ny}x{nzl}", "--steps", "3", "--warmup", "3", "--no-e2e",
+                          "--no-cpu-baseline", "--no-config1", "--seed", str(seed),
+                          "--transport", transport, "--dump", prefix],
+                         cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == world and len(line["ranks"]) == world
+    assert sorted(r["rank"] for r in line["ranks"]) == list(range(world))
+    assert line["config"]["halo_transport"] == transport and not line["peer_wait_timeout"]
+    assert line["dump"]["steps"] == 6
+
+    # the same initial state (bench.py: slab r from rng(seed + r)), whole lattice
+    model = lk.D3Q19Model()
+    full = lk.LatticeShape(nx, ny, nzl * world)
+    from paper_1405_6162_b200.lattice import FieldDescriptor, field_create
+
+    desc = FieldDescriptor.create(19, full.nsites)
+    f0, g0 = field_create(desc), field_create(desc)
+    for r in range(world):
+        fs, gs = random_binary_state(lk.LatticeShape(nx, ny, nzl), np.random.default_rng(seed + r),
+                                     model)
+        for dst, src in ((f0, fs), (g0, gs)):
+            for i in range(19):
+                d = dst.component(i).reshape(nx, ny, nzl * world)
+                d[:, :, r * nzl:(r + 1) * nzl] = src.component(i).reshape(nx, ny, nzl)
+    prm = orc.fluid_params(tau_f=1.0, tau_g=1.0, physics=1)
+    of, og, _, _ = orc.fluid_step(f0.data, g0.data, (nx, ny, nzl * world), desc.padded_sites,
+                                  prm, steps=6)
+    from paper_1405_6162_b200 import io as lio
+
+    fd, shape = lio.read_slab(prefix + ".f", 0, nzl * world)
+    gd, _ = lio.read_slab(prefix + ".g", 0, nzl * world)
+    assert shape == full
+    n = full.nsites
+    for got, ref in ((fd, of), (gd, og)):
+        assert np.array_equal(got.data.reshape(19, -1)[:, :n],
+                              ref.reshape(19, -1)[:, :n])
