@@ -383,12 +383,13 @@ def collision_config1(peak, peak_src, iters=50, vvls=(1, 2, 4, 8)):
                          "bytes_per_site": COLLISION_BYTES_PER_SITE}}
 
 
-def reference_collision_cpu(budget_s=3.0, vvls=(1, 2, 4, 8), n=128):
-    """The reference's OWN CPU path for configs[1]: latkit.bench.benchmark_run
-    (reference pkg/src/latkit/bench.py:49-101) over the numba _collision_range
-    (kernels.py:89-125), backend "threaded" with every host core, imported from
-    the unmodified install in baseline/_ref.  One untimed run absorbs the numba
-    JIT; iterations per VVL are sized to ~budget_s."""
+def reference_collision_cpu(budget_s=3.0, vvls=(1, 2, 4, 8), n=128, workers_list=None):
+    """The reference's OWN CPU path for the collision configs: latkit.bench.
+    benchmark_run (reference pkg/src/latkit/bench.py:49-101) over the numba
+    _collision_range (kernels.py:89-125), backend "threaded", imported from the
+    unmodified install in baseline/_ref.  One untimed run absorbs the numba
+    JIT; iterations per (workers, VVL) are sized to ~budget_s.  `value` is the
+    best VVL with every host core (BASELINE.md §3's plan: workers 1 and nproc)."""
     try:
         if REF_PKG not in sys.path:
             sys.path.insert(0, REF_PKG)
@@ -397,27 +398,29 @@ def reference_collision_cpu(budget_s=3.0, vvls=(1, 2, 4, 8), n=128):
         from latkit.lattice import LatticeShape as RefShape
     except Exception as exc:  # noqa: BLE001
         return {"unavailable": f"reference latkit not importable from baseline/_ref: {exc}"}
-    workers = os.cpu_count() or 1
+    ncpu = os.cpu_count() or 1
+    workers_list = workers_list or [ncpu]
     try:
         t0 = time.perf_counter()
-        ref_run("binary-collision", RefShape(16, 16, 16), 1, workers, "threaded", 1)
+        ref_run("binary-collision", RefShape(16, 16, 16), 1, ncpu, "threaded", 1)
         jit_s = time.perf_counter() - t0
         shape = RefShape(n, n, n)
         sweep = []
-        for v in vvls:
-            probe = ref_run("binary-collision", shape, v, workers, "threaded", 1)
-            iters = max(1, int(budget_s / max(probe.elapsed_s, 1e-6)))
-            r = ref_run("binary-collision", shape, v, workers, "threaded", iters)
-            sweep.append({"vvl": v, "iters": iters, "mlups": r.sites_per_s / 1e6,
-                          "gb_s": r.bandwidth_gb_s})
+        for w in workers_list:
+            for v in vvls:
+                probe = ref_run("binary-collision", shape, v, w, "threaded", 1)
+                iters = max(1, int(budget_s / max(probe.elapsed_s, 1e-6)))
+                r = ref_run("binary-collision", shape, v, w, "threaded", iters)
+                sweep.append({"workers": w, "vvl": v, "iters": iters,
+                              "mlups": r.sites_per_s / 1e6, "gb_s": r.bandwidth_gb_s})
     except Exception as exc:  # noqa: BLE001
         return {"unavailable": f"reference benchmark_run failed: {exc}"}
-    best = max(sweep, key=lambda d: d["mlups"])
-    return {"value": best["mlups"], "unit": "MLUPS", "cores": workers, "kind": "reference",
+    best = max((d for d in sweep if d["workers"] == max(workers_list)), key=lambda d: d["mlups"])
+    return {"value": best["mlups"], "unit": "MLUPS", "cores": best["workers"], "kind": "reference",
             "sample": f"{n}^3 binary-collision, latkit {getattr(latkit, '__version__', '?')} "
                       "benchmark_run (numba _collision_range), backend threaded, "
                       f"best of VVL {list(vvls)}; numba JIT {jit_s:.1f} s untimed",
-            "best_vvl": best["vvl"], "vvl_sweep": sweep}
+            "best_vvl": best["vvl"], "sweep": sweep}
 
 
 # ----------------------------------------------------------------- reference arm
@@ -457,8 +460,12 @@ def run_reference(args, rank, world):
                                    f"{steps} timesteps (oracle/lb_oracle.c orc_fluid_step)"},
         "e2e": {"value": mlups, "unit": "MLUPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        # BASELINE configs[1] on the reference's own code (numba), same box
-        "collision_128": None if args.no_config1 else reference_collision_cpu(),
+        # BASELINE configs[0] (32^3, the reference's CPU-runnable case) and configs[1]
+        # (128^3) on the reference's own code (numba), same box, workers 1 and nproc
+        "collision_32": None if args.no_config1 else reference_collision_cpu(
+            budget_s=1.0, n=32, workers_list=[1, os.cpu_count() or 1]),
+        "collision_128": None if args.no_config1 else reference_collision_cpu(
+            budget_s=2.0, workers_list=[1, os.cpu_count() or 1]),
     }
     print(json.dumps(line), flush=True)
     return 0
