@@ -95,6 +95,8 @@ def parse_args(argv=None):
     p.add_argument("--dump", default=None, metavar="PREFIX",
                    help="after the timed steps, write the lattice state (reference field "
                         "format, every rank its slab) to PREFIX.f / PREFIX.g (parity checks)")
+    p.add_argument("--no-variants", action="store_true",
+                   help="skip the tau 0.8 / FAST sub-record")
     p.add_argument("--no-config1", action="store_true",
                    help="skip the configs[1] collision-only 128^3 sub-record")
     p.add_argument("--seed", type=int, default=1234)
@@ -531,6 +533,7 @@ def run_ours(args, rank, world, local):
             transport = "nccl (peer transport unavailable)"
         ctl.barrier()  # every inbox reset before any neighbour primes it
     if transport.startswith("nccl"):
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator ranks visible in the log
         uid = lk.nccl_unique_id() if rank == 0 else None
         sim.attach_nccl(ctl.bcast_bytes(uid, 128))
     layout = "row" if sim.set_layout(None) == lk.LAYOUT_ROW else "soa"
@@ -615,6 +618,28 @@ def run_ours(args, rank, world, local):
         dump_state(sim, args.dump, ctl.barrier)
         dumped = {"prefix": args.dump, "steps": args.warmup + args.steps, "seed": args.seed}
 
+    # the same step off the easy case (the timed line is EXACT at tau = 1, whose
+    # x / 1.0 shortcut skips the relaxation divisions): EXACT at tau 0.8 (every
+    # division) and FAST, 10 steps each, same engine and state
+    variants = None
+    if not args.no_variants:
+        variants = {}
+        for name, mdl, md in (("exact_tau0.8", lk.D3Q19Model(tau_f=0.8, tau_g=0.8), lk.MODE_EXACT),
+                              ("fast", model, lk.MODE_FAST)):
+            sim.set_model(model=mdl, mode=md)
+            sim.run(2)
+            sim.sync()
+            ctl.barrier()
+            nat.check(nat.lib.ltk_event_record(start, sim.stream))
+            sim.run(10)
+            nat.check(nat.lib.ltk_event_record(stop, sim.stream))
+            sim.sync()
+            vms = ctl.allreduce(nat.elapsed_ms(start, stop), "MAX") / 10
+            variants[name] = {"ms_per_step": vms,
+                              "value": sites_rank * world / (vms * 1e-3) / 1e6}
+        sim.set_model(model=model, mode=mode)
+        sim.load(f0, g0)  # the timed configuration again, from the initial state
+
     # ---------------- e2e: public API with host buffers, every step
     e2e = e2e_job = None
     if not args.no_e2e and args.scaling == "weak":  # strong: 41 GB of state per 512^3 GPU
@@ -678,6 +703,7 @@ def run_ours(args, rank, world, local):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_job": e2e_job,
+            "variants": variants,
             "collision_128": coll,
             "dump": dumped,
         }

@@ -301,6 +301,18 @@ class BinaryFluid:
         tot = np.array(out[:])
         return allreduce(tot) if allreduce is not None else tot
 
+    def set_model(self, model: D3Q19Model | None = None, free_energy: FreeEnergy | None = None,
+                  physics: str | None = None, mode: int | None = None) -> None:
+        """Change relaxation times, free energy, force form or arithmetic mode
+        between steps (the state stays; later steps use the new parameters)."""
+        self.model = model or self.model
+        self.free_energy = free_energy or self.free_energy
+        self.physics = physics or self.physics
+        self.mode = self.mode if mode is None else mode
+        self._params = fluid_params(self.model, self.free_energy, self.physics, self.mode)
+        nat.check(nat.lib.ltk_fluid_set_params(self._h, ctypes.byref(self._params)),
+                  "ltk_fluid_set_params")
+
     # -- stepping ------------------------------------------------------------
 
     def run(self, nsteps: int, stream: int | None = None) -> None:
