@@ -1,6 +1,7 @@
 """Small engine runs for compute-sanitizer (memcheck / racecheck): every layout,
-force form, the fused step, VVL 2, the peer transport between in-process slabs
-and ragged plane counts for k_mu_blk.  Prints one line per case; exits 1 on a
+force form, VVL 2, the peer transport between in-process slabs, ragged plane
+counts for k_mu_tile (nzl not a multiple of its 8-plane blocks) and the plain
+mu kernel (ny % 8 != 0).  Prints one line per case; exits 1 on a
 result that differs from the single-slab SoA run.
 
     compute-sanitizer --tool memcheck python scripts/sanitize_engine.py
@@ -15,7 +16,7 @@ import paper_1405_6162_b200 as lk  # noqa: E402
 from paper_1405_6162_b200.kernels import random_binary_state  # noqa: E402
 
 
-def run(shape, layout, physics="binary", vvl=1, fuse=False, nslabs=1, steps=3):
+def run(shape, layout, physics="binary", vvl=1, nslabs=1, steps=3):
     full = lk.LatticeShape(*shape)
     model = lk.D3Q19Model(tau_f=0.9, tau_g=1.1)
     f0, g0 = random_binary_state(full, np.random.default_rng(5), model)
@@ -24,7 +25,6 @@ def run(shape, layout, physics="binary", vvl=1, fuse=False, nslabs=1, steps=3):
     try:
         for s in sims:
             s.set_layout(layout)
-            s.set_fuse(fuse, 1)
         if nslabs > 1:
             for r, s in enumerate(sims):
                 s.attach_peer_engines(sims[(r + 1) % nslabs], sims[(r - 1) % nslabs])
@@ -54,7 +54,8 @@ def main():
         dict(shape=(32, 8, 11), physics="binary-stress"),
         dict(shape=(32, 8, 11), physics="passive"),
         dict(shape=(32, 8, 12), vvl=2),
-        dict(shape=(32, 8, 12), fuse=True),
+        dict(shape=(32, 6, 12)),
+        dict(shape=(64, 16, 5), physics="binary-stress"),
         dict(shape=(16, 6, 12), nslabs=2),
         dict(shape=(16, 6, 12), nslabs=3, physics="binary-stress"),
     ]
