@@ -797,6 +797,15 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
     sim.sync()
     ms = nat.elapsed_ms(start, stop)
     ms_max = ctl.allreduce(ms, "MAX")
+    # every e2e step maps the same input state to the same result: the D2H'd
+    # result must equal one step of the plain public path (load, run, fields)
+    sim.load(f0, g0)
+    sim.run(1)
+    rf, rg = sim.fields(slab_only=world > 1)
+    ok = bool(np.array_equal(rf.data.view(np.uint64), of.view(np.uint64)) and
+              np.array_equal(rg.data.view(np.uint64), og.view(np.uint64)))
+    ok = ctl.allreduce(1.0 if ok else 0.0, "MIN") == 1.0
+    del rf, rg
     for p in stage_in + stage_out:
         nat.free(p)
     for s in set(h2d_st + d2h_st):
@@ -810,6 +819,7 @@ def run_e2e(args, sim, f0, g0, ctl, world, nat, lk):
             "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
             "steps": args.e2e_steps, "ms_per_step": ms_max / args.e2e_steps,
             "copy_streams_per_direction": S,
+            "result_bitwise_equal_to_public_step": ok,
             "path": "pinned H2D(f,g) -> BinaryFluid.load_device -> run(1) -> store_device -> "
                     "D2H(f,g); separate double-buffered input/result staging, so step k+1's "
                     "H2D and step k's D2H stream concurrently, each split over "

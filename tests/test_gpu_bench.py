@@ -46,6 +46,9 @@ def test_bench_line_contract():
     e = d["e2e"]
     nb = 2 * 19 * 64 * 64 * 32 * 8  # f and g of the slab, padded == nsites here
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == nb and e["d2h_bytes_per_step"] == nb
+    # the chunked multi-stream pipeline returns exactly one public-API step
+    assert e["copy_streams_per_direction"] == 4
+    assert e["result_bitwise_equal_to_public_step"] is True
     k = d["clocks"]
     assert "sm_mhz" in k and "reasons" in k
 
