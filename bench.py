@@ -387,6 +387,29 @@ def collision_config1(peak, peak_src, iters=50, vvls=(1, 2, 4, 8)):
                          "bytes_per_site": COLLISION_BYTES_PER_SITE}}
 
 
+def collision_config0(iters=200, vvls=(1, 2, 4, 8)):
+    """BASELINE configs[0] on the GPU: the reference collision at 32^3 (the
+    reference's CPU-runnable case) through the same latkit-API benchmark_run.
+    The 5 MB state sits in L2 and a launch moves 20 MB in a few microseconds,
+    so this line measures the per-launch cost of the drop-in path (Python
+    launch() -> ctypes -> kernel), not HBM."""
+    import paper_1405_6162_b200 as lk
+    from paper_1405_6162_b200.bench import benchmark_run
+
+    shape = lk.LatticeShape(32, 32, 32)
+    sweep = []
+    for v in vvls:
+        r = benchmark_run("binary-collision", shape, v, iterations=iters, mode=lk.MODE_EXACT)
+        sweep.append({"vvl": v, "us_per_launch": r.elapsed_s / iters * 1e6,
+                      "mlups": r.sites_per_s / 1e6})
+    best = max(sweep, key=lambda d: d["mlups"])
+    return {"workload": "BASELINE configs[0]: binary-collision kernel, 32^3 fp64, EXACT "
+                        f"(bitwise = reference), latkit benchmark_run, {iters} launches per VVL "
+                        "(launch-bound: the state is L2-resident)",
+            "vvl_sweep": sweep, "best_vvl": best["vvl"], "value": best["mlups"],
+            "unit": "MLUPS", "bound": "launch"}
+
+
 def reference_collision_cpu(budget_s=3.0, vvls=(1, 2, 4, 8), n=128, workers_list=None):
     """The reference's OWN CPU path for the collision configs: latkit.bench.
     benchmark_run (reference pkg/src/latkit/bench.py:49-101) over the numba
@@ -659,11 +682,13 @@ def run_ours(args, rank, world, local):
                          f"timesteps ({dt:.1f} s), oracle/lb_oracle.c orc_fluid_step"}
 
     sim.close()
-    coll = None
+    coll = coll0 = None
     if rank == 0 and world == 1 and not args.no_config1:
         coll = collision_config1(peak, peak_src)
+        coll0 = collision_config0()
         if not args.no_cpu_baseline:
             coll["cpu_baseline"] = reference_collision_cpu()
+            coll0["cpu_baseline"] = reference_collision_cpu(budget_s=1.0, n=32)
     if rank == 0:
         line = {
             "metric": "lattice site updates/sec (MLUPS), D3Q19 binary-fluid full timestep",
@@ -707,6 +732,7 @@ def run_ours(args, rank, world, local):
             "e2e_job": e2e_job,
             "variants": variants,
             "collision_128": coll,
+            "collision_32": coll0,
             "dump": dumped,
         }
         print(json.dumps(line), flush=True)

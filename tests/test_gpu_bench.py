@@ -51,6 +51,13 @@ def test_bench_line_contract():
     assert e["result_bitwise_equal_to_public_step"] is True
     k = d["clocks"]
     assert "sm_mhz" in k and "reasons" in k
+    # BASELINE configs[1] and configs[0] sub-records on the device, each next to
+    # the reference's own numba CPU number (or the reason it is unavailable)
+    for key, n in (("collision_128", 128), ("collision_32", 32)):
+        c = d[key]
+        assert c["value"] > 0 and [r["vvl"] for r in c["vvl_sweep"]] == [1, 2, 4, 8], key
+        cb = c["cpu_baseline"]
+        assert ("unavailable" in cb) or (cb["kind"] == "reference" and f"{n}^3" in cb["sample"])
 
 
 def test_bench_line_stress_form_bytes():

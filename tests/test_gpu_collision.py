@@ -315,6 +315,40 @@ class TestEdgeCases:
                               orc._p(orc.CV.astype(float)), orc.CS2, 1.0, 1.0, 40, 80)
         assert np.array_equal(out.data, rf)
 
+    def test_prepared_parameters_follow_constant_updates(self, lk):
+        # launch() reuses the prepared parameter block between identical launches;
+        # a constant update between launches (tau_f 1.0 -> 0.8) must reach the
+        # kernel, and a launch on other buffers must use those buffers
+        from oracle import oracle as orc
+
+        f0, g0 = _state(lk, (8, 8, 8), 11)
+        P, n = f0.descriptor.padded_sites, f0.descriptor.nsites
+        dev = lk.TargetDevice()
+        lk.set_model_constants(dev, lk.D3Q19Model())
+        bufs = [lk.target_malloc(dev, f0.descriptor) for _ in range(4)]
+        for b, src in zip(bufs, (f0, g0, f0, g0)):
+            lk.copy_to_target(b, src)
+        plan = lk.LaunchPlan(extent=P, vvl=2)
+        lk.launch(dev, lk.binary_collision_kernel, plan, bufs[:2])
+        lk.sync_target(dev)
+        dev.constant_set_double("tau_f", 0.8)
+        lk.launch(dev, lk.binary_collision_kernel, plan, bufs[:2])
+        lk.sync_target(dev)
+        lk.launch(dev, lk.binary_collision_kernel, plan, bufs[2:])  # same constants, other buffers
+        lk.sync_target(dev)
+        got = []
+        for b in bufs:
+            out = lk.field_create(f0.descriptor)
+            lk.copy_from_target(out, b)
+            got.append(out.data)
+        rf, rg = f0.data.copy(), g0.data.copy()
+        orc.collide(rf, rg, P, n, tau_f=1.0, tau_g=1.0)
+        orc.collide(rf, rg, P, n, tau_f=0.8, tau_g=1.0)
+        sf, sg = f0.data.copy(), g0.data.copy()
+        orc.collide(sf, sg, P, n, tau_f=0.8, tau_g=1.0)
+        assert np.array_equal(got[0], rf) and np.array_equal(got[1], rg)
+        assert np.array_equal(got[2], sf) and np.array_equal(got[3], sg)
+
     def test_nan_input_propagates_like_reference(self, lk):
         from oracle import oracle as orc
         from paper_1405_6162_b200.verify import run_framework_collision
