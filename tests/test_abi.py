@@ -96,3 +96,21 @@ int main(void) {
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stderr
     assert out.stdout.startswith("abi 2")
+
+
+def test_nccl_shim_covers_the_engines_nccl_symbols(tmp_path):
+    # the stand-in libnccl.so.2 of tests/nccl_shim (GPU test of the NCCL slab path
+    # with P >= 2 ranks on one device) exports every symbol fluid.cu dlsym's
+    src = open(os.path.join(ROOT, "paper_1405_6162_b200", "csrc", "fluid.cu")).read()
+    wanted = set(re.findall(r'dlsym\(n\.h, "(nccl\w+)"\)', src))
+    assert len(wanted) == 8
+    out = tmp_path / "libnccl.so.2"
+    subprocess.run(["g++", "-O2", "-fPIC", "-shared", "-Wl,-soname,libnccl.so.2",
+                    "-I/usr/local/cuda/include", "-o", str(out),
+                    os.path.join(ROOT, "tests", "nccl_shim", "nccl_shim.cpp"),
+                    "-L/usr/local/cuda/lib64", "-lcudart_static", "-ldl", "-lrt", "-lpthread"],
+                   check=True, capture_output=True)
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(out)], capture_output=True,
+                        text=True, check=True).stdout
+    exported = {line.split()[-1] for line in nm.splitlines() if " T " in line}
+    assert wanted <= exported, wanted - exported
