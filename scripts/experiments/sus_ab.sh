@@ -1,3 +1,5 @@
+# A/B of libltk.so vs libltk_ng.so (built with -DLTK_NOGUARD: div_rcp without its inf/NaN
+# pass-through; the macro was removed again after this measurement).
 cd "${GRAFT_REPO_ROOT}"
 mkdir -p gpurun_out; rm -f gpurun_out/sus_ab.txt
 cp paper_1405_6162_b200/_native/libltk.so /tmp/libltk_guard.so
