@@ -85,7 +85,7 @@ def parse_args(argv=None):
                         "star), the momentum-conserving stress divergence, or none")
     p.add_argument("--tau", type=float, default=1.0,
                    help="tau_f = tau_g (reference default 1.0, model.py:48-49)")
-    p.add_argument("--e2e-steps", type=int, default=48,
+    p.add_argument("--e2e-steps", type=int, default=96,
                    help="e2e steps (pipeline fill/drain of one H2D + one D2H is amortised "
                         "over them)")
     p.add_argument("--e2e-streams", type=int, choices=(1, 2, 4, 8), default=4,
