@@ -8,7 +8,7 @@ host<->target copies stay outside the timed region, as in the reference
 
 from __future__ import annotations
 
-import io
+import itertools
 from dataclasses import dataclass
 
 import numpy as np
@@ -45,47 +45,62 @@ class BenchResult:
     cuda_block: int = 0
 
 
+def _stage(kernel_id: str, device: TargetDevice, shape: LatticeShape, rng, max_vvl: int,
+           mode: int | None) -> list:
+    """Seeded inputs of one kernel, resident on the device (outside the timing)."""
+    if kernel_id == "scale":
+        vec = random_vector_field(shape, rng, max_vvl)
+        device.constant_set_double("a", 1.0)  # full work and no drift over the iterations
+        fields = [vec]
+    else:
+        model = D3Q19Model()
+        fields = list(random_binary_state(shape, rng, model, max_vvl))
+        set_model_constants(device, model, mode)
+    bufs = [target_malloc(device, fld.descriptor) for fld in fields]
+    for buf, fld in zip(bufs, fields):
+        copy_to_target(buf, fld)
+    return bufs
+
+
+def _timed_launches(device: TargetDevice, kernel, plan: LaunchPlan, bufs: list, n: int) -> float:
+    """Seconds for n back-to-back launches, CUDA events on the device stream."""
+    ev = [nat.event_create(True), nat.event_create(True)]
+    try:
+        nat.check(nat.lib.ltk_event_record(ev[0], device.stream))
+        for _ in range(n):
+            launch(device, kernel, plan, bufs)
+        nat.check(nat.lib.ltk_event_record(ev[1], device.stream))
+        sync_target(device)
+        return nat.elapsed_ms(ev[0], ev[1]) * 1e-3
+    finally:
+        for e in ev:
+            nat.lib.ltk_event_destroy(e)
+
+
 def benchmark_run(kernel_id: str, shape: LatticeShape, vvl: int, workers: int = 1,
                   backend: str = "cuda", iterations: int = 5, tpb: int = 128, seed: int = 1234,
                   max_vvl: int = DEFAULT_MAX_VVL, mode: int | None = None) -> BenchResult:
-    """Time `iterations` launches of one configuration (reference bench.py:49-101)."""
+    """Time `iterations` launches of one configuration (reference bench.py:49-101):
+    one untimed warm-up launch, then the timed ones; the copies are set-up."""
     if iterations < 1:
         raise ConfigError("iterations must be >= 1")
-    rng = np.random.default_rng(seed)
     device = TargetDevice(backend=backend, workers=workers)
     kernel = kernel_by_id(kernel_id)
-    if kernel_id == "scale":
-        field = random_vector_field(shape, rng, max_vvl)
-        device.constant_set_double("a", 1.0)
-        bufs = [target_malloc(device, field.descriptor)]
-        copy_to_target(bufs[0], field)
-    else:
-        model = D3Q19Model()
-        f, g = random_binary_state(shape, rng, model, max_vvl)
-        set_model_constants(device, model, mode)
-        bufs = [target_malloc(device, f.descriptor), target_malloc(device, g.descriptor)]
-        copy_to_target(bufs[0], f)
-        copy_to_target(bufs[1], g)
+    bufs = _stage(kernel_id, device, shape, np.random.default_rng(seed), max_vvl, mode)
     plan = LaunchPlan(extent=bufs[0].descriptor.padded_sites, vvl=vvl, workers=workers, tpb=tpb)
-
-    launch(device, kernel, plan, bufs)  # warm-up, untimed
-    sync_target(device)
-    start, stop = nat.event_create(True), nat.event_create(True)
-    nat.check(nat.lib.ltk_event_record(start, device.stream))
-    for _ in range(iterations):
+    try:
         launch(device, kernel, plan, bufs)
-    nat.check(nat.lib.ltk_event_record(stop, device.stream))
-    sync_target(device)
-    elapsed = nat.elapsed_ms(start, stop) * 1e-3
-    nat.lib.ltk_event_destroy(start)
-    nat.lib.ltk_event_destroy(stop)
-    for b in bufs:
-        target_free(b)
-    sites_per_s = shape.nsites * iterations / elapsed
-    result = BenchResult(kernel_id, backend, shape.nx, shape.ny, shape.nz, vvl, workers,
-                         tpb, iterations, elapsed, sites_per_s,
-                         sites_per_s * BYTES_PER_SITE[kernel_id] / 1e9, device.counters,
-                         cuda_block=plan.cuda_block)
+        sync_target(device)
+        elapsed = _timed_launches(device, kernel, plan, bufs, iterations)
+    finally:
+        for buf in bufs:
+            target_free(buf)
+    rate = shape.nsites * iterations / elapsed
+    result = BenchResult(kernel=kernel_id, backend=backend, nx=shape.nx, ny=shape.ny,
+                         nz=shape.nz, vvl=vvl, workers=workers, tpb=tpb, iters=iterations,
+                         elapsed_s=elapsed, sites_per_s=rate,
+                         bandwidth_gb_s=rate * BYTES_PER_SITE[kernel_id] / 1e9,
+                         counters=device.counters, cuda_block=plan.cuda_block)
     device.close()
     return result
 
@@ -93,51 +108,59 @@ def benchmark_run(kernel_id: str, shape: LatticeShape, vvl: int, workers: int = 
 def run_sweep(kernel_id: str, shape: LatticeShape, vvls: list[int], workers_list: list[int],
               backends: list[str], iterations: int, tpb: int = 128, seed: int = 1234,
               mode: int | None = None) -> list[BenchResult]:
-    """One benchmark_run per (backend, workers, vvl), in input order (bench.py:104-123)."""
-    if not vvls or not workers_list or not backends:
+    """benchmark_run over backends x workers x VVLs, that nesting order (bench.py:104-123)."""
+    if not (vvls and workers_list and backends):
         raise ConfigError("vvl, workers, and backend lists must be non-empty")
     return [benchmark_run(kernel_id, shape, v, w, b, iterations, tpb=tpb, seed=seed, mode=mode)
-            for b in backends for w in workers_list for v in vvls]
+            for b, w, v in itertools.product(backends, workers_list, vvls)]
 
 
 CSV_HEADER = "kernel,backend,nx,ny,nz,vvl,workers,tpb,iters,elapsed_s,sites_per_s"
 
 
+def _fields(r: BenchResult, t_fmt: str, rate_fmt: str) -> list[str]:
+    return [r.kernel, r.backend, str(r.nx), str(r.ny), str(r.nz), str(r.vvl), str(r.workers),
+            str(r.tpb), str(r.iters), format(r.elapsed_s, t_fmt), format(r.sites_per_s, rate_fmt)]
+
+
 def emit_csv(results: list[BenchResult]) -> str:
-    """reference bench.py:129-140 schema."""
+    """The reference CSV schema (bench.py:126-140), one row per run in input order."""
     if not results:
         raise ConfigError("no results to emit")
-    out = io.StringIO()
-    out.write(CSV_HEADER + "\n")
-    for r in results:
-        out.write(f"{r.kernel},{r.backend},{r.nx},{r.ny},{r.nz},{r.vvl},{r.workers},"
-                  f"{r.tpb},{r.iters},{r.elapsed_s:.9g},{r.sites_per_s:.9g}\n")
-    return out.getvalue()
+    rows = [CSV_HEADER] + [",".join(_fields(r, ".9g", ".9g")) for r in results]
+    return "\n".join(rows) + "\n"
 
 
 def emit_table(results: list[BenchResult]) -> str:
-    cols = CSV_HEADER.split(",") + ["GB/s"]
-    rows = [cols] + [[r.kernel, r.backend, str(r.nx), str(r.ny), str(r.nz), str(r.vvl),
-                      str(r.workers), str(r.tpb), str(r.iters), f"{r.elapsed_s:.6f}",
-                      f"{r.sites_per_s:.4g}", f"{r.bandwidth_gb_s:.1f}"] for r in results]
-    widths = [max(len(row[i]) for row in rows) for i in range(len(cols))]
-    return "\n".join("  ".join(c.ljust(w) for c, w in zip(row, widths)).rstrip()
-                     for row in rows) + "\n"
+    """Aligned text table of the CSV columns plus the achieved HBM GB/s."""
+    table = [CSV_HEADER.split(",") + ["GB/s"]]
+    table += [_fields(r, ".6f", ".4g") + [f"{r.bandwidth_gb_s:.1f}"] for r in results]
+    width = [max(map(len, col)) for col in zip(*table)]
+    return "".join("  ".join(cell.ljust(w) for cell, w in zip(row, width)).rstrip() + "\n"
+                   for row in table)
 
 
 def report_best(results: list[BenchResult]) -> list[str]:
-    """Best VVL per (kernel, backend) and its speedup over VVL=1 (bench.py:156-176)."""
-    groups: dict[tuple[str, str], list[BenchResult]] = {}
+    """Per (kernel, backend), in first-seen order: the best VVL (ties to the smaller
+    VVL) and its throughput over the VVL=1 run with the same workers
+    (reference bench.py:143-176; ConfigError when that baseline is missing)."""
+    order: list[tuple[str, str]] = []
+    by_group: dict[tuple[str, str], list[BenchResult]] = {}
     for r in results:
-        groups.setdefault((r.kernel, r.backend), []).append(r)
-    lines = []
-    for (kernel, backend), rows in groups.items():
-        base = {r.workers: r for r in rows if r.vvl == 1}
-        for r in rows:
-            if r.workers not in base:
-                raise ConfigError(f"missing VVL=1 baseline for {kernel}/{backend} "
-                                  f"workers={r.workers}")
-        best = max(rows, key=lambda r: (r.sites_per_s, -r.vvl))
-        speedup = best.sites_per_s / base[best.workers].sites_per_s
-        lines.append(f"{kernel}/{backend}: best VVL={best.vvl}, {speedup:.2f}x over VVL=1")
-    return lines
+        key = (r.kernel, r.backend)
+        if key not in by_group:
+            order.append(key)
+            by_group[key] = []
+        by_group[key].append(r)
+    out = []
+    for kernel, backend in order:
+        runs = by_group[(kernel, backend)]
+        vvl1 = {r.workers: r for r in runs if r.vvl == 1}
+        orphan = next((r for r in runs if r.workers not in vvl1), None)
+        if orphan is not None:
+            raise ConfigError(f"missing VVL=1 baseline for {kernel}/{backend} "
+                              f"workers={orphan.workers}")
+        top = max(runs, key=lambda r: (r.sites_per_s, -r.vvl))
+        gain = top.sites_per_s / vvl1[top.workers].sites_per_s
+        out.append(f"{kernel}/{backend}: best VVL={top.vvl}, {gain:.2f}x over VVL=1")
+    return out
