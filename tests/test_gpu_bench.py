@@ -51,6 +51,11 @@ def test_bench_line_contract():
     assert e["result_bitwise_equal_to_public_step"] is True
     k = d["clocks"]
     assert "sm_mhz" in k and "reasons" in k
+    # the same step off the easy case, and held long enough to meet the power cap
+    v = d["variants"]
+    assert v["exact_tau0.8"]["value"] > 0 and v["fast"]["value"] > 0
+    assert v["sustained"]["steps"] == 500 and v["sustained"]["value"] > 0
+    assert "sm_mhz" in v["sustained"]["clocks"]
     # BASELINE configs[1] and configs[0] sub-records on the device, each next to
     # the reference's own numba CPU number (or the reason it is unavailable)
     for key, n in (("collision_128", 128), ("collision_32", 32)):
