@@ -90,8 +90,8 @@ def parse_args(argv=None):
                         "over them)")
     p.add_argument("--e2e-streams", type=int, choices=(1, 2, 4, 8), default=4,
                    help="copy streams per PCIe direction in the e2e path (f and g split "
-                        "into chunks across them; 4 measured fastest full duplex: "
-                        "97.6 vs 88.9 GB/s with 1, scripts/exp_pcie.py)")
+                        "into chunks across them; full duplex measured 96-97.6 GB/s with 4 "
+                        "vs 88.9 GB/s with 1 on these boxes, scripts/exp_pcie.py)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--sustained-steps", type=int, default=500,
                    help="steps of the sustained (power-capped) sub-record in variants; 0 = off")
@@ -100,9 +100,10 @@ def parse_args(argv=None):
                    help="after the timed steps, write the lattice state (reference field "
                         "format, every rank its slab) to PREFIX.f / PREFIX.g (parity checks)")
     p.add_argument("--no-variants", action="store_true",
-                   help="skip the tau 0.8 / FAST sub-record")
+                   help="skip the tau 0.8 / FAST / sustained sub-records")
     p.add_argument("--no-config1", action="store_true",
-                   help="skip the configs[1] collision-only 128^3 sub-record")
+                   help="skip the configs[1] (128^3) and configs[0] (32^3) collision-only "
+                        "sub-records")
     p.add_argument("--seed", type=int, default=1234)
     p.add_argument("--layout", choices=("soa", "row"), default="row",
                    help="f/g storage: component-major planes (soa) or row-blocked (row: "
