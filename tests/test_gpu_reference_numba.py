@@ -79,3 +79,41 @@ def test_scale_bitwise_vs_reference_numba(ref, lk):
     v = random_vector_field(lk.LatticeShape(*shape), np.random.default_rng(7))
     got = run_framework_scale(v, 0.37, "threaded", 4, 1)
     assert np.array_equal(got.data.view(np.uint64), want.data.view(np.uint64))
+
+
+def test_passive_step_equals_reference_collision_after_streaming(ref, lk):
+    # the engine's full step in the passive limit (no force, no chemical potential) is
+    # the reference collision applied to the pulled (streamed) state: three steps at 64^3
+    # against numpy streaming + the reference's own numba collision, bitwise
+    from paper_1405_6162_b200.kernels import random_binary_state
+
+    shape = (64, 64, 64)
+    nx, ny, nz = shape
+    n = nx * ny * nz
+    model = lk.D3Q19Model(tau_f=0.9, tau_g=1.2)
+    f0, g0 = random_binary_state(lk.LatticeShape(*shape), np.random.default_rng(11), model)
+    with lk.BinaryFluid(lk.LatticeShape(*shape), model=model, physics="passive") as sim:
+        sim.load(f0, g0)
+        sim.run(3)
+        f1, g1 = sim.fields()
+    P = f0.descriptor.padded_sites
+    cv = np.asarray(model.cv, dtype=int)
+
+    def stream(a):  # f_i(x) <- f_i(x - c_i), host order s = (x*ny + y)*nz + z, periodic
+        out = a.copy().reshape(19, P)
+        for i in range(19):
+            v = out[i, :n].reshape(nx, ny, nz)
+            out[i, :n] = np.roll(v, tuple(cv[i]), axis=(0, 1, 2)).ravel()
+        return out.ravel()
+
+    rmodel = ref.D3Q19Model(tau_f=0.9, tau_g=1.2)
+    rdesc = ref.FieldDescriptor.create(19, n)
+    rf = ref.Field(rdesc, f0.data.copy())
+    rg = ref.Field(rdesc, g0.data.copy())
+    for _ in range(3):
+        rf = ref.Field(rdesc, stream(rf.data))
+        rg = ref.Field(rdesc, stream(rg.data))
+        rf, rg = ref.verify.run_framework_collision(rf, rg, "threaded", 1, os.cpu_count() or 1,
+                                                    model=rmodel)
+    assert np.array_equal(f1.data.view(np.uint64), rf.data.view(np.uint64))
+    assert np.array_equal(g1.data.view(np.uint64), rg.data.view(np.uint64))
