@@ -413,6 +413,38 @@ def collision_config0(iters=200, vvls=(1, 2, 4, 8)):
             "unit": "MLUPS", "bound": "launch"}
 
 
+def reference_parity_128(steps=1, seed=20140707):
+    """configs[1] parity in the bench line: one collision of the 128^3 state on the
+    device (EXACT, through the latkit API) against the reference's own numba
+    code run through ITS launch API on the host cores (baseline/_ref install).
+    A checker only: its time is not part of any rate."""
+    try:
+        if REF_PKG not in sys.path:
+            sys.path.insert(0, REF_PKG)
+        import latkit.kernels
+        import latkit.verify
+    except Exception as exc:  # noqa: BLE001
+        return {"unavailable": f"reference latkit not importable from baseline/_ref: {exc}"}
+    import numpy as np
+
+    import paper_1405_6162_b200 as lk
+    from paper_1405_6162_b200.kernels import random_binary_state
+    from paper_1405_6162_b200.verify import run_framework_collision
+
+    n = 128
+    rf0, rg0 = latkit.kernels.random_binary_state(latkit.LatticeShape(n, n, n),
+                                                  np.random.default_rng(seed),
+                                                  latkit.D3Q19Model())
+    rf, rg = latkit.verify.run_framework_collision(rf0, rg0, "threaded", 1, os.cpu_count() or 1,
+                                                   steps=steps)
+    f0, g0 = random_binary_state(lk.LatticeShape(n, n, n), np.random.default_rng(seed))
+    f1, g1 = run_framework_collision(f0, g0, "cuda", 1, 1, steps=steps, mode=lk.MODE_EXACT)
+    same = bool(np.array_equal(f1.data.view(np.uint64), rf.data.view(np.uint64)) and
+                np.array_equal(g1.data.view(np.uint64), rg.data.view(np.uint64)))
+    return {"shape": f"{n}^3", "steps": steps, "seed": seed,
+            "bitwise_equal_to_reference_numba": same}
+
+
 def reference_collision_cpu(budget_s=3.0, vvls=(1, 2, 4, 8), n=128, workers_list=None):
     """The reference's OWN CPU path for the collision configs: latkit.bench.
     benchmark_run (reference pkg/src/latkit/bench.py:49-101) over the numba
@@ -708,6 +740,7 @@ def run_ours(args, rank, world, local):
         coll0 = collision_config0()
         if not args.no_cpu_baseline:
             coll["cpu_baseline"] = reference_collision_cpu()
+            coll["parity"] = reference_parity_128()
             coll0["cpu_baseline"] = reference_collision_cpu(budget_s=1.0, n=32)
     if rank == 0:
         line = {

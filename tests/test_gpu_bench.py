@@ -61,6 +61,9 @@ def test_bench_line_contract():
     for key, n in (("collision_128", 128), ("collision_32", 32)):
         c = d[key]
         assert c["value"] > 0 and [r["vvl"] for r in c["vvl_sweep"]] == [1, 2, 4, 8], key
+        if key == "collision_128":
+            par = c["parity"]
+            assert ("unavailable" in par) or par["bitwise_equal_to_reference_numba"] is True
         cb = c["cpu_baseline"]
         assert ("unavailable" in cb) or (cb["kind"] == "reference" and f"{n}^3" in cb["sample"])
 
