@@ -439,3 +439,61 @@ class TestExactDivision:
         assert np.array_equal(np.isnan(got), nan)
         same = got[~nan].view(np.uint64) == ref[~nan].view(np.uint64)
         assert same.all(), (x[~nan][~same][:5], d[~nan][~same][:5])
+
+
+class TestLaunchSequences:
+    def test_random_launch_sequences_match_oracle(self, lk):
+        # launch() reuses the prepared parameter block while (kernel, plan, buffers,
+        # constants) are unchanged: random interleavings of constant updates, plan
+        # changes and buffer pairs on one device must still give the oracle's bits
+        import os
+
+        from hypothesis import given, settings
+        from hypothesis import strategies as st
+
+        from oracle import oracle as orc
+
+        shape = lk.LatticeShape(6, 5, 4)
+        f0, g0 = _state(lk, (6, 5, 4), 21)
+        P, n = f0.descriptor.padded_sites, f0.descriptor.nsites
+        op = st.one_of(
+            st.tuples(st.just("tau_f"), st.sampled_from([0.7, 0.8, 1.0, 1.3])),
+            st.tuples(st.just("tau_g"), st.sampled_from([0.6, 1.0, 1.7])),
+            st.tuples(st.just("launch"), st.integers(0, 1), st.sampled_from([1, 2, 4, 8, 16]),
+                      st.sampled_from([32, 64, 128, 256])))
+
+        @settings(max_examples=int(os.environ.get("LTK_HYP_EXAMPLES", "30")), deadline=None)
+        @given(ops=st.lists(op, min_size=1, max_size=12))
+        def run(ops):
+            dev = lk.TargetDevice()
+            try:
+                lk.set_model_constants(dev, lk.D3Q19Model())
+                pairs = []
+                for _ in range(2):
+                    bf = lk.target_malloc(dev, f0.descriptor)
+                    bg = lk.target_malloc(dev, g0.descriptor)
+                    lk.copy_to_target(bf, f0)
+                    lk.copy_to_target(bg, g0)
+                    pairs.append((bf, bg))
+                host = [(f0.data.copy(), g0.data.copy()) for _ in range(2)]
+                tau = {"tau_f": 1.0, "tau_g": 1.0}
+                for o in ops:
+                    if o[0] in tau:
+                        dev.constant_set_double(o[0], o[1])
+                        tau[o[0]] = o[1]
+                        continue
+                    _, k, vvl, tpb = o
+                    plan = lk.LaunchPlan(extent=P, vvl=vvl, tpb=tpb)
+                    lk.launch(dev, lk.binary_collision_kernel, plan, list(pairs[k]))
+                    lk.sync_target(dev)
+                    orc.collide(host[k][0], host[k][1], P, n, tau_f=tau["tau_f"],
+                                tau_g=tau["tau_g"])
+                for (bf, bg), (hf, hg) in zip(pairs, host):
+                    out_f, out_g = lk.field_create(f0.descriptor), lk.field_create(g0.descriptor)
+                    lk.copy_from_target(out_f, bf)
+                    lk.copy_from_target(out_g, bg)
+                    assert np.array_equal(out_f.data, hf) and np.array_equal(out_g.data, hg)
+            finally:
+                dev.close()
+
+        run()
